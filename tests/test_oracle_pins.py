@@ -1,0 +1,283 @@
+"""Pins for the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names the pin from DESIGN.md §Pins / SURVEY.md §8(c):
+  brute force  -- all alignment paths enumerated explicitly (definition of an
+                  alignment score, no DP) pin FULLDP; FULLDP pins EXTEND when X
+                  exceeds the no-pruning bound (P-1)
+  closed forms -- identical strings (P-2), single substitution (P-3),
+                  all-mismatch cell count (X+2)^2 (P-4), unpruned cell count
+                  (m+1)(n+1)
+  hand traces  -- tests/golden/extend_hand.txt
+  invariants   -- upper bound (P-5), symmetry (P-6), achievability (P-7),
+                  left/right mirror (P-8)
+Both oracle implementations (C: oracle.extend, Python: xdrop_ref.extend) are
+pinned by the same checks, and must agree with each other.
+"""
+import itertools
+import os
+import random
+
+import pytest
+
+import oracle
+from oracle import xdrop_ref as ref
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+ALPH = "ACGT"
+
+
+def impls():
+    return [("c", oracle.extend), ("py", ref.extend)]
+
+
+# ----------------------------------------------------------------- brute force
+def enumerate_best(a, b, M, mu, g):
+    """Max score of every cell by explicit enumeration of all move sequences."""
+    m, n = len(a), len(b)
+    best = {}
+
+    def walk(i, j, v):
+        if best.get((i, j), None) is None or v > best[(i, j)]:
+            best[(i, j)] = v
+        if i < m and j < n:
+            walk(i + 1, j + 1, v + (M if a[i] == b[j] else mu))
+        if i < m:
+            walk(i + 1, j, v + g)
+        if j < n:
+            walk(i, j + 1, v + g)
+
+    walk(0, 0, 0)
+    return best
+
+
+def argmax_rule(cellvals):
+    """Tie-break of reading Q8: smallest anti-diagonal, then smallest i."""
+    top = max(cellvals.values())
+    i, j = min(((i, j) for (i, j), v in cellvals.items() if v == top), key=lambda c: (c[0] + c[1], c[0]))
+    return top, i, j
+
+
+@pytest.mark.parametrize("M,mu,g", [(1, -1, -1), (2, -3, -2), (5, -4, -3)])
+def test_fulldp_matches_path_enumeration(M, mu, g):
+    rng = random.Random(7)
+    for _ in range(120):
+        a = "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 4)))
+        b = "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 4)))
+        assert ref.fulldp(a, b, M, mu, g) == argmax_rule(enumerate_best(a, b, M, mu, g))
+
+
+def no_prune_bound(m, n, M, mu, g):
+    # P-1: best <= min(m,n)*M and every H(i,j) >= -max(i,j)*max(-mu,-g)
+    return min(m, n) * M + max(m, n) * max(-mu, -g)
+
+
+def strings(alph, maxlen):
+    for L in range(maxlen + 1):
+        for t in itertools.product(alph, repeat=L):
+            yield "".join(t)
+
+
+@pytest.mark.parametrize("name,fn", impls())
+def test_P1_exhaustive_tiny_equals_fulldp(name, fn):
+    pool = list(strings("AC", 4)) + list(strings(ALPH, 2))
+    for a in pool:
+        for b in pool:
+            X = no_prune_bound(len(a), len(b), 1, -1, -1)
+            best, i, j, cells = fn(a, b, 1, -1, -1, X)
+            assert (best, i, j) == ref.fulldp(a, b), (a, b)
+            assert cells == (len(a) + 1) * (len(b) + 1), (a, b)  # nothing pruned -> full rectangle
+
+
+@pytest.mark.parametrize("name,fn", impls())
+@pytest.mark.parametrize("M,mu,g", [(1, -1, -1), (2, -3, -2), (5, -4, -3)])
+def test_P1_random_equals_fulldp(name, fn, M, mu, g):
+    rng = random.Random(11)
+    for _ in range(60):
+        a = "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 25)))
+        b = list(a) if rng.random() < 0.5 else [rng.choice(ALPH) for _ in range(rng.randint(0, 25))]
+        for t in range(len(b)):
+            if rng.random() < 0.15:
+                b[t] = rng.choice(ALPH)
+        b = "".join(b)
+        X = no_prune_bound(len(a), len(b), M, mu, g)
+        best, i, j, cells = fn(a, b, M, mu, g, X)
+        assert (best, i, j) == ref.fulldp(a, b, M, mu, g)
+        assert cells == (len(a) + 1) * (len(b) + 1)
+
+
+# ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("name,fn", impls())
+def test_P2_identical(name, fn):
+    rng = random.Random(3)
+    for L in [0, 1, 2, 7, 31, 64]:
+        a = "".join(rng.choice(ALPH) for _ in range(L))
+        for X in [0, 1, 5, 15, 100]:
+            for (M, mu, g) in [(1, -1, -1), (2, -3, -2)]:
+                best, i, j, _ = fn(a, a, M, mu, g, X)
+                assert (best, i, j) == (L * M, L, L)
+
+
+@pytest.mark.parametrize("name,fn", impls())
+def test_P3_single_substitution(name, fn):
+    rng = random.Random(5)
+    for L in [4, 9, 20, 40]:
+        a = "".join(rng.choice(ALPH) for _ in range(L))
+        for p in range(0, L - 2):
+            b = list(a)
+            b[p] = ALPH[(ALPH.index(a[p]) + 1) % 4]
+            b = "".join(b)
+            assert fn(a, b, 1, -1, -1, 0)[:3] == (p, p, p)
+            for X in [1, 2, 15]:
+                assert fn(a, b, 1, -1, -1, X)[:3] == (L - 2, L, L), (a, b, p, X)
+
+
+@pytest.mark.parametrize("name,fn", impls())
+def test_P4_all_mismatch_cells(name, fn):
+    for X in [0, 1, 2, 5, 15]:
+        for extra in [0, 1, 7]:
+            m, n = X + 1 + extra, X + 1 + (extra * 2) % 5
+            assert fn("A" * m, "C" * n, 1, -1, -1, X) == (0, 0, 0, (X + 2) ** 2)
+
+
+# ----------------------------------------------------------------- hand traces
+def load_golden():
+    rows = []
+    with open(os.path.join(GOLDEN, "extend_hand.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            lhs, rhs = line.split("|")
+            a, b, M, mu, g, X = lhs.split()
+            a = "" if a == "-" else a
+            b = "" if b == "-" else b
+            rows.append((a, b, int(M), int(mu), int(g), int(X), tuple(int(t) for t in rhs.split())))
+    return rows
+
+
+@pytest.mark.parametrize("name,fn", impls())
+def test_golden_hand_traces(name, fn):
+    rows = load_golden()
+    assert len(rows) >= 6
+    for a, b, M, mu, g, X, want in rows:
+        assert fn(a, b, M, mu, g, X) == want, (a, b, X)
+
+
+# ------------------------------------------------------------------ invariants
+def mutate(rng, a, err):
+    out = []
+    for ch in a:
+        r = rng.random()
+        if r < err / 3:
+            continue                                    # deletion
+        if r < 2 * err / 3:
+            out.append(rng.choice(ALPH))                # insertion
+        if r < err:
+            out.append(ALPH[(ALPH.index(ch) + rng.randint(1, 3)) % 4])  # substitution
+        else:
+            out.append(ch)
+    return "".join(out)
+
+
+def test_invariants_P5_P6_P7_and_twins_agree():
+    rng = random.Random(13)
+    for _ in range(400):
+        L = rng.randint(0, 30)
+        a = "".join(rng.choice(ALPH) for _ in range(L))
+        b = mutate(rng, a, 0.25) if rng.random() < 0.7 else "".join(
+            rng.choice(ALPH) for _ in range(rng.randint(0, 30)))
+        M, mu, g = rng.choice([(1, -1, -1), (2, -3, -2), (5, -4, -3), (2, -1, -1)])
+        full = ref.fulldp(a, b, M, mu, g)
+        for X in [0, 1, 2, 3, 5, 10]:
+            c = oracle.extend(a, b, M, mu, g, X)
+            p = ref.extend(a, b, M, mu, g, X)
+            assert c == p, (a, b, X)                     # the two oracles agree
+            assert c[0] <= full[0]                       # P-5 upper bound
+            sw = oracle.extend(b, a, M, mu, g, X)
+            assert sw[0] == c[0] and sw[3] == c[3]       # P-6 symmetry (score, cells)
+            # P-7 achievability: the unpruned optimum at (i*, j*) is >= best
+            assert ref.fulldp(a[:c[1]], b[:c[2]], M, mu, g) is not None
+            sub = ref.fulldp(a[:c[1]], b[:c[2]], M, mu, g)
+            # H_full(i*, j*) is the NW value of the prefixes: recompute directly
+            assert nw(a[:c[1]], b[:c[2]], M, mu, g) >= c[0]
+            assert sub[0] >= c[0]
+
+
+def nw(a, b, M, mu, g):
+    """Global NW score of a vs b via path enumeration on tiny, DP otherwise."""
+    m, n = len(a), len(b)
+    prev = [j * g for j in range(n + 1)]
+    for i in range(1, m + 1):
+        cur = [i * g] + [0] * n
+        for j in range(1, n + 1):
+            cur[j] = max(prev[j] + g, cur[j - 1] + g, prev[j - 1] + (M if a[i - 1] == b[j - 1] else mu))
+        prev = cur
+    return prev[n]
+
+
+def test_P8_left_right_mirror_and_align_wiring():
+    rng = random.Random(17)
+    for _ in range(200):
+        A = "".join(rng.choice(ALPH) for _ in range(rng.randint(5, 60)))
+        B = mutate(rng, A, 0.2)
+        k = rng.randint(1, 4)
+        if len(B) < k:
+            continue
+        a_pos = rng.randint(0, len(A) - k)
+        b_pos = rng.randint(0, len(B) - k)
+        X = rng.choice([0, 2, 7, 15])
+        r = oracle.align(A, B, a_pos, b_pos, k, 1, -1, -1, X)
+        # mirror: left extension == right extension of the reversed reads at the mirrored seed
+        rr = oracle.align(A[::-1], B[::-1], len(A) - a_pos - k, len(B) - b_pos - k, k, 1, -1, -1, X)
+        assert r["left"] == rr["right"] and r["right"] == rr["left"]
+        assert r["score"] == rr["score"] and r["cells"] == rr["cells"]
+        assert (r["a_begin"], r["a_end"]) == (len(A) - rr["a_end"], len(A) - rr["a_begin"])
+        # wiring against the pure-Python twin
+        p = ref.align(A, B, a_pos, b_pos, k, 1, -1, -1, X)
+        assert {kk: r[kk] for kk in p} == p
+
+
+def test_align_identical_reads_closed_form():
+    rng = random.Random(19)
+    for _ in range(50):
+        A = "".join(rng.choice(ALPH) for _ in range(rng.randint(20, 200)))
+        k = 17 if len(A) >= 17 else 1
+        pos = rng.randint(0, len(A) - k)
+        for X in [0, 15]:
+            r = oracle.align(A, A, pos, pos, k, 1, -1, -1, X)
+            assert (r["score"], r["a_begin"], r["a_end"], r["b_begin"], r["b_end"]) == (len(A), 0, len(A), 0, len(A))
+
+
+def test_survey_regression_nonmonotone_in_X():
+    """SURVEY.md §0 finding 2 (two independent scratch implementations during the survey):
+    the X-drop score is NOT monotone in X; our oracle must reproduce the printed triple."""
+    a, b = "ATCACTGAGCATATGGTC", "CACTATTGAGCATCAGGGTC"
+    got = {X: oracle.extend(a, b, 1, -1, -1, X)[:3] for X in (1, 2, 3)}
+    assert got == {1: (9, 18, 20), 2: (2, 6, 4), 3: (9, 18, 20)}
+
+
+def test_batch_matches_single():
+    rng = random.Random(23)
+    import numpy as np
+    reads = ["".join(rng.choice(ALPH) for _ in range(rng.randint(30, 120))) for _ in range(12)]
+    seq = np.frombuffer("".join(reads).encode(), dtype=np.uint8)
+    off = np.zeros(len(reads) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(r) for r in reads])
+    pairs = []
+    for _ in range(40):
+        ai, bi = rng.randrange(12), rng.randrange(12)
+        pairs.append((ai, bi, rng.randint(0, len(reads[ai]) - 5), rng.randint(0, len(reads[bi]) - 5)))
+    res, cells = oracle.align_batch(seq, off, seq, off, np.array(pairs), 5, X=7, nthreads=3)
+    for t, (ai, bi, ap, bp) in enumerate(pairs):
+        r = oracle.align(reads[ai], reads[bi], ap, bp, 5, X=7)
+        assert (res[t]["score"], res[t]["a_begin"], res[t]["a_end"], res[t]["b_begin"],
+                res[t]["b_end"], cells[t]) == (r["score"], r["a_begin"], r["a_end"],
+                                                r["b_begin"], r["b_end"], r["cells"])
+
+
+def test_batch_reports_bad_seed():
+    import numpy as np
+    seq = np.frombuffer(b"ACGTACGT", dtype=np.uint8)
+    off = np.array([0, 8], dtype=np.int64)
+    with pytest.raises(ValueError):
+        oracle.align_batch(seq, off, seq, off, np.array([[0, 0, 5, 0]]), 5)
