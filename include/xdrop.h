@@ -1,0 +1,197 @@
+/*
+ * include/xdrop.h -- C ABI of the B200-native batched X-drop seed-and-extend
+ * library (libxdrop.so, built from paper_2309_07270_b200/csrc/).
+ *
+ * What the library computes
+ * -------------------------
+ * For each candidate read pair with a shared k-mer seed it runs ALIGN:
+ *   seed  = sum_{t<k} s(A[a_pos+t], B[b_pos+t])
+ *   R     = EXTEND(A[a_pos+k:], B[b_pos+k:])                 (right extension)
+ *   L     = EXTEND(reverse(A[:a_pos]), reverse(B[:b_pos]))   (left extension)
+ * where EXTEND is the anti-diagonal X-drop dynamic program: cells of one
+ * anti-diagonal d = i + j are independent (§II on LOGAN), a cell
+ * is dead when its value falls below (best over anti-diagonals < d) - X
+ * ("X-drop"; "--ga 15"), and the
+ * recurrence is Needleman-Wunsch with linear gaps ("essentially
+ * Needleman-Wunsch or Smith-Waterman algorithm with X-Drop").
+ * Every detail the paper leaves open (tie-breaks, hull, termination, seed
+ * score, coordinates) is fixed in DESIGN.md "Readings"; the
+ * CPU oracle in oracle/ implements the same reading independently.
+ *
+ * Conventions
+ * -----------
+ * - Every function returns XDROP_OK (0) or a negative xdrop_status; nothing
+ *   throws across the ABI.  xdrop_strerror() names a status.
+ * - Ownership: the caller owns every buffer it passes (host or device) and
+ *   every output buffer; the library owns its device workspaces and streams.
+ *   xdrop_align_batch is synchronous: inputs may be freed on return and `out`
+ *   is complete.
+ * - On error the outputs are unspecified and xdrop_last_error_index() returns
+ *   the offending pair index (EINVAL/ESEED/ELENGTH) or pool base index
+ *   (EALPHABET), else -1.
+ * - Determinism: results are bit-identical across runs, policies, device
+ *   counts and kernel paths (the result never depends on the band window).
+ * - Thread safety: one context per host thread, or serialise calls.
+ */
+#ifndef XDROP_H_
+#define XDROP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  XDROP_OK = 0,
+  XDROP_EINVAL = -1,     /* bad argument (null pointer, bad params, bad id) */
+  XDROP_ENOMEM = -2,     /* host or device allocation failed */
+  XDROP_ECUDA = -3,      /* CUDA runtime error */
+  XDROP_EALPHABET = -4,  /* a base outside {A,C,G,T,a,c,g,t} ("--alph dna") */
+  XDROP_ESEED = -5,      /* seed out of range: a_pos<0, a_pos+k>|A| (same for B) */
+  XDROP_ELENGTH = -6,    /* a read longer than XDROP_MAX_READ_LEN, or score range exceeded */
+  XDROP_ESTATE = -7,     /* call on a finalized / null context */
+  XDROP_ENODEV = -8      /* no usable CUDA device */
+} xdrop_status;
+
+/* Rank->GPU mapping policies.  CELLS is the default sharding by estimated cell
+ * count; the other three re-create the paper's schedulers (§III-B..D,
+ * Alg. 1 l.5-30): ONE2ALL = one logical rank at a time drives all GPUs,
+ * ONE2ONE = rank r drives GPU r mod m with per-pipeline token rings (token per
+ * sub-batch), OPT_ONE2ONE = as ONE2ONE with the token held per batch
+ * (BASELINE.json's "mixed scheme").  Results never depend on the policy. */
+typedef enum {
+  XDROP_POLICY_CELLS = 0,
+  XDROP_POLICY_ONE2ALL = 1,
+  XDROP_POLICY_ONE2ONE = 2,
+  XDROP_POLICY_OPT_ONE2ONE = 3
+} xdrop_policy;
+
+#define XDROP_MAX_READ_LEN (1 << 18) /* bases per read (fast-path key range) */
+
+/* Scoring and X-drop parameters.  Valid ranges: 1 <= match <= 32,
+ * -64 <= mismatch <= -1, -64 <= gap <= -1, 0 <= xdrop <= 2^20,
+ * 1 <= k <= 1024.  BASELINE: {+1, -1, -1, 15, 17}; the paper ran k=31, X=15
+ * (PAPER.md:221, 224). */
+typedef struct {
+  int32_t match, mismatch, gap, xdrop, k;
+} xdrop_params;
+
+typedef struct {
+  const int* devices;   /* CUDA device ordinals; NULL -> device 0 .. n_devices-1 */
+  int n_devices;        /* >= 1 */
+  int policy;           /* xdrop_policy */
+  int n_ranks;          /* logical ranks for ONE2ALL/ONE2ONE/OPT (>= 1); ignored by CELLS */
+  int batch_size;       /* pairs per batch, PAPER.md:100 ("batches of size 10,000"); 0 -> 10000 */
+  int subbatches;       /* c sub-batches per batch; 0 -> 1 */
+  int flags;            /* XDROP_FLAG_* */
+} xdrop_init_opts;
+
+#define XDROP_FLAG_FORCE_WIDE 1    /* skip the lane-per-extension path (tests) */
+#define XDROP_FLAG_FORCE_GENERAL 2 /* send every extension to the unbounded fallback (tests) */
+#define XDROP_FLAG_NO_SORT 4       /* do not length-sort the work queue (tests) */
+
+/* A read pool in HOST memory: ASCII bases, read r = seq[offsets[r] .. offsets[r+1]). */
+typedef struct {
+  const char* seq;
+  const int64_t* offsets; /* n + 1 entries, non-decreasing, offsets[0] >= 0 */
+  int64_t n;              /* number of reads */
+} xdrop_seqs;
+
+/* One candidate pair: seed A[a_pos, a_pos+k) ~ B[b_pos, b_pos+k).  16 bytes. */
+typedef struct {
+  int32_t a_id, b_id, a_pos, b_pos;
+} xdrop_pair;
+
+/* Result of ALIGN, 0-based half-open coordinates [begin, end).  20 bytes. */
+typedef struct {
+  int32_t score, a_begin, a_end, b_begin, b_end;
+} xdrop_result;
+
+typedef struct xdrop_ctx xdrop_ctx;
+
+/* Create a context over opts->n_devices GPUs (NULL opts: 1 GPU, CELLS). */
+int xdrop_init(const xdrop_init_opts* opts, xdrop_ctx** out_ctx);
+
+/* Align n_pairs pairs (host buffers).  B may equal A (same pool).  out has
+ * n_pairs entries; cells_out (nullable) receives per-pair DP cell counts
+ * (hull cells of the left + right extensions). */
+int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
+                      const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                      xdrop_result* out, int64_t* cells_out);
+
+/* Device-resident variant on the context's first device: every pointer is
+ * device memory (e.g. torch tensors' data_ptr()).  seqA/offA describe an ASCII
+ * pool of nA reads with total length lenA (= offA[nA], passed so no D2H read
+ * is needed); seqB may equal seqA.  Work is enqueued on `stream`
+ * (cudaStream_t, NULL = the context's stream); the call returns after the
+ * stream has completed so it can report validation errors. */
+int xdrop_align_batch_device(xdrop_ctx* ctx,
+                             const char* seqA, const int64_t* offA, int64_t nA, int64_t lenA,
+                             const char* seqB, const int64_t* offB, int64_t nB, int64_t lenB,
+                             const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                             xdrop_result* out, int64_t* cells_out, void* stream);
+
+/* Counters of the last call on this context (first device). */
+typedef struct {
+  int64_t items;          /* extensions (2 per pair) */
+  int64_t escalated[4];   /* extensions that reached path level 1, 2, 3 (general) */
+  int64_t cells;          /* total DP cells */
+  float kernel_ms;        /* CUDA-event time of the alignment kernels (all levels) */
+  float total_ms;         /* CUDA-event time of the whole device pipeline */
+  float pack_ms;          /* ASCII -> 2-bit pack kernel */
+  int64_t launches;       /* kernels launched by the last call */
+  float level_ms[4];      /* CUDA-event time of each band level (0: lane/extension, 1-2: warp/extension, 3: general) */
+  int64_t level_cells[4]; /* DP cells of the extensions completed at each level */
+  int64_t level_items[4]; /* extensions completed at each level */
+} xdrop_stats;
+int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
+
+/* ---- scheduler observability (§III; SPEC.md verify semantics) ---- */
+typedef struct {
+  int32_t rank, gpu, batch, sub;  /* logical rank, device slot, 1-based batch / sub-batch (0 for CELLS) */
+  int64_t n_pairs;
+  double t0_ms, t1_ms;            /* host wall clock relative to the call start */
+} xdrop_trace_event;
+
+typedef struct {
+  int64_t handoffs;       /* token messages (Alg. 1 l.30 MPI_Send(True,[right])) */
+  int64_t exchange_msgs;  /* batch-count exchange messages (Alg. 1 l.5-11) */
+  int64_t turns;          /* sub-batch executions (events in the trace) */
+  double span_ms;         /* first turn start to last turn end ("alignment time", Table I) */
+  double busy_ms[16];     /* per device slot */
+  int32_t max_concurrent; /* most turns running at one instant */
+  int32_t n_events;       /* events recorded for xdrop_last_trace */
+} xdrop_sched_stats;
+
+int xdrop_last_sched_stats(const xdrop_ctx* ctx, xdrop_sched_stats* st);
+/* Copy up to cap events of the last call's trace; returns the number available. */
+int64_t xdrop_last_trace(const xdrop_ctx* ctx, xdrop_trace_event* buf, int64_t cap);
+
+/* Host-only dry run of a policy (no GPU needed): every turn "runs" for
+ * ns_per_unit * sum(w) nanoseconds of sleep.  gpu_of_pair (nullable, n
+ * entries) receives the device slot that ran each pair.  Returns the number of
+ * trace events (<= cap copied to trace) or a negative status. */
+int64_t xdrop_sched_simulate(int m, int policy, int n_ranks, int batch_size, int subbatches,
+                             const int64_t* w, int64_t n, double ns_per_unit, xdrop_sched_stats* st,
+                             xdrop_trace_event* trace, int64_t cap, int32_t* gpu_of_pair);
+
+/* Alg. 1 ring search over ranks 0..n-1: first rank r,
+ * walking down (left) / up (right) from `rank` with wrap-around, with
+ * batch <= counts[r]; -1 when the walk returns to `rank`. */
+int xdrop_ring_left(int rank, int batch, const int* counts, int n);
+int xdrop_ring_right(int rank, int batch, const int* counts, int n);
+
+int xdrop_finalize(xdrop_ctx* ctx);
+const char* xdrop_strerror(int status);
+int64_t xdrop_last_error_index(const xdrop_ctx* ctx);
+
+/* Measure the INT32 issue rate of the first device (ops/s) with a dependent-
+ * chain-free IADD3/LOP3/IMNMX/IMAD mix; fills ops_per_s[0] = ALU-pipe-only mix,
+ * ops_per_s[1] = ALU+FMA-pipe mix.  Used only to cross-check the roofline. */
+int xdrop_int32_peak(xdrop_ctx* ctx, double* ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XDROP_H_ */

@@ -1,0 +1,162 @@
+"""B200-native batched X-drop seed-and-extend (arxiv 2309.07270's hot path).
+
+Public API: :class:`Aligner` (wraps the C ABI in include/xdrop.h).  PyTorch is
+used only for device memory and streams (``align_device``); every step of the
+path runs in the CUDA kernels of ``libxdrop.so``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from ._native import RESULT_DTYPE, TRACE_DTYPE, XdropError  # noqa: F401
+
+__all__ = ["Aligner", "XdropError", "RESULT_DTYPE", "TRACE_DTYPE", "ring_left", "ring_right",
+           "sched_simulate"]
+
+
+def _params(M, mu, g, X, k):
+    return N.Params(int(M), int(mu), int(g), int(X), int(k))
+
+
+class Aligner:
+    """A context over one or more GPUs (``xdrop_init``)."""
+
+    def __init__(self, n_devices: int = 1, devices=None, policy: str = "cells", n_ranks: int = 1,
+                 batch_size: int = 10000, subbatches: int = 1, flags: int = 0):
+        opts = N.InitOpts()
+        self._dev_arr = None
+        if devices is not None:
+            self._dev_arr = (ctypes.c_int * len(devices))(*devices)
+            opts.devices = ctypes.cast(self._dev_arr, ctypes.POINTER(ctypes.c_int))
+            n_devices = len(devices)
+        opts.n_devices = n_devices
+        opts.policy = N.POLICIES[policy] if isinstance(policy, str) else int(policy)
+        opts.n_ranks, opts.batch_size, opts.subbatches, opts.flags = n_ranks, batch_size, subbatches, flags
+        h = ctypes.c_void_p()
+        N.check(N.lib.xdrop_init(ctypes.byref(opts), ctypes.byref(h)), "xdrop_init")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.xdrop_finalize(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---------------------------------------------------------------- host API
+    def align(self, seqA: np.ndarray, offA: np.ndarray, pairs: np.ndarray, k: int, X: int,
+              M: int = 1, mu: int = -1, g: int = -1, seqB=None, offB=None, want_cells: bool = True):
+        """xdrop_align_batch on host buffers -> (results RESULT_DTYPE[n], cells int64[n])."""
+        seqA = np.ascontiguousarray(seqA, dtype=np.uint8)
+        offA = np.ascontiguousarray(offA, dtype=np.int64)
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 4)
+        A = N.Seqs(seqA.ctypes.data, offA.ctypes.data, offA.shape[0] - 1)
+        if seqB is None:
+            B = A
+            pB = ctypes.byref(A)
+        else:
+            seqB = np.ascontiguousarray(seqB, dtype=np.uint8)
+            offB = np.ascontiguousarray(offB, dtype=np.int64)
+            B = N.Seqs(seqB.ctypes.data, offB.ctypes.data, offB.shape[0] - 1)
+            pB = ctypes.byref(B)
+        n = pairs.shape[0]
+        out = np.zeros(n, dtype=RESULT_DTYPE)
+        cells = np.zeros(n, dtype=np.int64) if want_cells else None
+        p = _params(M, mu, g, X, k)
+        st = N.lib.xdrop_align_batch(self._h, ctypes.byref(A), pB, pairs.ctypes.data, n, ctypes.byref(p),
+                                     out.ctypes.data, cells.ctypes.data if want_cells else None)
+        N.check(st, "xdrop_align_batch", self._h)
+        return out, cells
+
+    # -------------------------------------------------------------- device API
+    def align_device(self, seqA, offA, pairs, out, cells, k: int, X: int, M: int = 1, mu: int = -1,
+                     g: int = -1, seqB=None, offB=None, lenA: int | None = None, lenB: int | None = None,
+                     stream=None):
+        """xdrop_align_batch_device on torch CUDA tensors (uint8 pool, int64 offsets,
+        int32[n,4] pairs, int32[n,5] out, int64[n] cells or None)."""
+        nA = offA.shape[0] - 1
+        if lenA is None:
+            lenA = int(seqA.shape[0])
+        if seqB is None:
+            seqB, offB, nB, lenB = seqA, offA, nA, lenA
+        else:
+            nB = offB.shape[0] - 1
+            lenB = int(seqB.shape[0]) if lenB is None else lenB
+        p = _params(M, mu, g, X, k)
+        s = stream.cuda_stream if stream is not None else None
+        st = N.lib.xdrop_align_batch_device(
+            self._h, seqA.data_ptr(), offA.data_ptr(), nA, lenA, seqB.data_ptr(), offB.data_ptr(), nB, lenB,
+            pairs.data_ptr(), pairs.shape[0], ctypes.byref(p), out.data_ptr(),
+            cells.data_ptr() if cells is not None else None, s)
+        N.check(st, "xdrop_align_batch_device", self._h)
+
+    # ------------------------------------------------------------ observability
+    def stats(self) -> dict:
+        s = N.Stats()
+        N.check(N.lib.xdrop_last_stats(self._h, ctypes.byref(s)), "xdrop_last_stats")
+        return dict(items=s.items, escalated=list(s.escalated), kernel_ms=s.kernel_ms, total_ms=s.total_ms,
+                    pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
+                    level_cells=list(s.level_cells), level_items=list(s.level_items))
+
+    def sched_stats(self) -> dict:
+        s = N.SchedStats()
+        N.check(N.lib.xdrop_last_sched_stats(self._h, ctypes.byref(s)), "xdrop_last_sched_stats")
+        return dict(handoffs=s.handoffs, exchange_msgs=s.exchange_msgs, turns=s.turns, span_ms=s.span_ms,
+                    busy_ms=list(s.busy_ms), max_concurrent=s.max_concurrent)
+
+    def trace(self) -> np.ndarray:
+        n = N.lib.xdrop_last_trace(self._h, None, 0)
+        buf = np.zeros(max(n, 0), dtype=TRACE_DTYPE)
+        if n > 0:
+            N.lib.xdrop_last_trace(self._h, buf.ctypes.data, n)
+        return buf
+
+    def int32_peak(self):
+        out = np.zeros(2, dtype=np.float64)
+        N.check(N.lib.xdrop_int32_peak(self._h, out.ctypes.data), "xdrop_int32_peak")
+        return float(out[0]), float(out[1])
+
+
+def ring_left(rank: int, batch: int, counts) -> int | None:
+    """Alg. 1 l.18-24 left-predecessor search (None when the walk returns to rank)."""
+    c = np.ascontiguousarray(counts, dtype=np.int32)
+    r = N.lib.xdrop_ring_left(rank, batch, c.ctypes.data, c.shape[0])
+    return None if r < 0 else r
+
+
+def ring_right(rank: int, batch: int, counts) -> int | None:
+    """Alg. 1 l.26-30 right-successor search."""
+    c = np.ascontiguousarray(counts, dtype=np.int32)
+    r = N.lib.xdrop_ring_right(rank, batch, c.ctypes.data, c.shape[0])
+    return None if r < 0 else r
+
+
+def sched_simulate(m: int, policy: str, n_ranks: int, w, batch_size: int = 10000, subbatches: int = 1,
+                   ns_per_unit: float = 0.0):
+    """Host-only dry run of a scheduling policy -> (trace, stats, gpu_of_pair)."""
+    w = np.ascontiguousarray(w, dtype=np.int64)
+    n = w.shape[0]
+    cap = 4 * (n // max(1, batch_size) + 2) * max(1, n_ranks) * max(1, subbatches) * max(1, m) + 64
+    trace = np.zeros(cap, dtype=TRACE_DTYPE)
+    gpu = np.full(n, -1, dtype=np.int32)
+    st = N.SchedStats()
+    r = N.lib.xdrop_sched_simulate(m, N.POLICIES[policy], n_ranks, batch_size, subbatches, w.ctypes.data, n,
+                                   ns_per_unit, ctypes.byref(st), trace.ctypes.data, cap, gpu.ctypes.data)
+    if r < 0:
+        raise XdropError(int(r), "xdrop_sched_simulate")
+    stats = dict(handoffs=st.handoffs, exchange_msgs=st.exchange_msgs, turns=st.turns, span_ms=st.span_ms,
+                 max_concurrent=st.max_concurrent)
+    return trace[:min(r, cap)], stats, gpu

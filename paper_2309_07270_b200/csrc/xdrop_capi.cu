@@ -1,0 +1,597 @@
+// xdrop_capi.cu -- host runtime and C ABI of libxdrop.so (include/xdrop.h).
+//
+// Layers: L2 per-device runtime (workspaces, streams, the
+// device pipeline pack -> prep/sort -> band levels -> combine), L3 multi-GPU
+// scheduler (sched.h: CELLS sharding + the paper's one2all / one2one /
+// opt_one2one policies, §III), L4 the C ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/xdrop.h"
+#include "sched.h"
+#include "xdrop_kernels.cuh"
+
+namespace {
+
+using xk::ExtOut;
+using xk::PairDesc;
+
+// ----------------------------------------------------------------- device ctx
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr; cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    want = want + want / 4;
+    if (cudaMalloc(&p, want) != cudaSuccess) { cudaGetLastError(); return XDROP_ENOMEM; }
+    cap = want;
+    return 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFreeHost(p);
+    p = nullptr; cap = 0;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) { cudaGetLastError(); return XDROP_ENOMEM; }
+    cap = bytes;
+    return 0;
+  }
+  void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
+};
+
+// counters block layout (ints)
+enum { C_NITEMS = 0, C_HEAD0 = 1, C_HEAD1 = 2, C_HEAD2 = 3, C_HEAD3 = 4, C_OVF1 = 5, C_OVF2 = 6, C_OVF3 = 7,
+       C_N = 8 };
+
+__global__ void init_counters_kernel(int* c, int n_items) {
+  if (threadIdx.x < C_N) c[threadIdx.x] = (threadIdx.x == C_NITEMS) ? n_items : 0;
+}
+__global__ void init_bad_kernel(unsigned long long* bad) {
+  if (threadIdx.x < 2) bad[threadIdx.x] = ~0ull;
+}
+
+struct DevCtx {
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1;
+  // device workspaces
+  Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
+      counters, bad, ext, out5, cells, scratch, level_acc;
+  // host staging
+  HostBuf h_small;
+  cudaEvent_t ev[12] = {};
+  xdrop_stats st{};
+  int64_t err_index = -1;
+};
+
+int cuda_err(cudaError_t e) {
+  if (e == cudaSuccess) return 0;
+  if (e == cudaErrorMemoryAllocation) return XDROP_ENOMEM;
+  return XDROP_ECUDA;
+}
+
+#define CK(x) do { int _r = cuda_err(x); if (_r) return _r; } while (0)
+#define CKR(x) do { int _r = (x); if (_r) return _r; } while (0)
+
+int dev_open(DevCtx& D, int dev) {
+  D.dev = dev;
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  D.sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
+  D.own_stream = true;
+  for (auto& e : D.ev) CK(cudaEventCreate(&e));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l0, xk::band_kernel<1, 32>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_kernel<32, 32>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_gen, xk::general_kernel, 128, 0));
+  D.occ_l0 = std::max(1, D.occ_l0); D.occ_l1 = std::max(1, D.occ_l1);
+  D.occ_l2 = std::max(1, D.occ_l2); D.occ_gen = std::max(1, D.occ_gen);
+  CKR(D.h_small.ensure(256));
+  return 0;
+}
+
+void dev_close(DevCtx& D) {
+  cudaSetDevice(D.dev);
+  if (D.stream) cudaStreamSynchronize(D.stream);
+  Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
+                 &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
+                 &D.cells, &D.scratch, &D.level_acc};
+  for (Buf* b : bufs) b->release();
+  D.h_small.release();
+  for (auto& e : D.ev) if (e) cudaEventDestroy(e);
+  if (D.own_stream && D.stream) cudaStreamDestroy(D.stream);
+  D.stream = nullptr;
+}
+
+int64_t packed_words(int64_t len) { return (len + 2 * xk::GUARD + 15) / 16 + 2; }
+
+int pack_pool(DevCtx& D, const char* d_seq, int64_t len, Buf& out, cudaStream_t s, int64_t& launches) {
+  const int64_t nw = packed_words(len);
+  CKR(out.ensure((size_t)nw * 4));
+  CK(cudaMemsetAsync(out.p, 0, (size_t)nw * 4, s));
+  const int64_t work = (len + xk::GUARD + 15) / 16;
+  const int thr = 256;
+  if (work > 0) {
+    xk::pack_kernel<<<(unsigned)((work + thr - 1) / thr), thr, 0, s>>>(d_seq, len, out.as<uint32_t>(),
+                                                                      D.bad.as<unsigned long long>());
+    ++launches;
+  }
+  return cuda_err(cudaGetLastError());
+}
+
+struct Flags { bool force_wide, force_general, nosort; };
+
+// The device pipeline on one GPU.  All pointers are device pointers.
+// out5 / cells may be the caller's buffers (device API) or D's workspaces.
+int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, int64_t lenA,
+                 const char* seqB, const int64_t* offB, int64_t nB, int64_t lenB,
+                 const PairDesc* pairs, int64_t n_pairs, const xdrop_params& p, int* out5,
+                 long long* cells, cudaStream_t s, Flags fl, bool do_pack = true) {
+  D.err_index = -1;
+  D.st = xdrop_stats{};
+  int64_t launches = 0;
+  CK(cudaSetDevice(D.dev));
+  const int64_t n_items = 2 * n_pairs;
+  CKR(D.bad.ensure(16));
+  CKR(D.counters.ensure(C_N * sizeof(int)));
+  CKR(D.hist.ensure(xk::NBUCKET * sizeof(int)));
+  CKR(D.cursor.ensure(xk::NBUCKET * sizeof(int)));
+  CKR(D.wcost.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+  CKR(D.items.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+  CKR(D.ovf1.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+  CKR(D.ovf2.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+  CKR(D.ovf3.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+  CKR(D.ext.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(ExtOut)));
+  CKR(D.level_acc.ensure(8 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(D.level_acc.p, 0, 8 * sizeof(unsigned long long), s));
+
+  CK(cudaEventRecord(D.ev[0], s));
+  init_bad_kernel<<<1, 32, 0, s>>>(D.bad.as<unsigned long long>());
+  init_counters_kernel<<<1, 32, 0, s>>>(D.counters.as<int>(), (int)n_items);
+  launches += 2;
+  // a1: ingest + pack (once per call per device; sub-batches reuse it)
+  if (do_pack) CKR(pack_pool(D, seqA, lenA, D.packA, s, launches));
+  const uint32_t* PB = D.packA.as<uint32_t>();
+  if (seqB != seqA) {
+    if (do_pack) CKR(pack_pool(D, seqB, lenB, D.packB, s, launches));
+    PB = D.packB.as<uint32_t>();
+  }
+  CK(cudaEventRecord(D.ev[1], s));
+
+  xk::Problem P;
+  P.PA = D.packA.as<uint32_t>(); P.offA = offA; P.nA = nA;
+  P.PB = PB; P.offB = offB; P.nB = nB;
+  P.pairs = pairs; P.n_pairs = n_pairs;
+  P.M = p.match; P.mu = p.mismatch; P.g = p.gap; P.X = p.xdrop; P.k = p.k;
+  P.ext = D.ext.as<ExtOut>();
+
+  int* ctr = D.counters.as<int>();
+  if (n_pairs > 0) {
+    // a2 + a3: validate, cost estimate, length-sorted queue
+    CK(cudaMemsetAsync(D.hist.p, 0, xk::NBUCKET * sizeof(int), s));
+    xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
+        P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
+    xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>());
+    xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
+        D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
+    launches += 3;
+  }
+  CK(cudaEventRecord(D.ev[2], s));
+  if (n_pairs > 0) {
+    // a5/a6/a7: band levels.  Level 0 = lane per extension (S = 32); level 1 =
+    // warp per extension (S = 256); level 2 = warp per extension (S = 1024).
+    int* items0 = D.items.as<int>();
+    int* lvl1_items = D.ovf1.as<int>();
+    int* lvl1_count = ctr + C_OVF1;
+    if (fl.force_wide || fl.force_general) {
+      lvl1_items = items0;
+      lvl1_count = ctr + C_NITEMS;
+    } else {
+      xk::band_kernel<1, 32><<<D.sms * D.occ_l0, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEAD0,
+                                                             D.ovf1.as<int>(), ctr + C_OVF1, 0);
+      ++launches;
+    }
+    CK(cudaEventRecord(D.ev[8], s));
+    int* gen_items = D.ovf3.as<int>();
+    int* gen_count = ctr + C_OVF3;
+    if (fl.force_general) {
+      gen_items = items0;
+      gen_count = ctr + C_NITEMS;
+    } else {
+      xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, lvl1_items, lvl1_count, ctr + C_HEAD1,
+                                                             D.ovf2.as<int>(), ctr + C_OVF2, 1);
+      CK(cudaEventRecord(D.ev[9], s));
+      xk::band_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, D.ovf2.as<int>(), ctr + C_OVF2,
+                                                              ctr + C_HEAD2, D.ovf3.as<int>(), ctr + C_OVF3, 2);
+      launches += 2;
+    }
+    if (fl.force_general) CK(cudaEventRecord(D.ev[9], s));
+    CK(cudaEventRecord(D.ev[10], s));
+    CK(cudaGetLastError());
+    // read the validation flags and the general-path count
+    int* hs = reinterpret_cast<int*>(D.h_small.p);
+    CK(cudaMemcpyAsync(hs, ctr, C_N * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + 16, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + 16);
+    if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
+    if (bad[1] != ~0ull) { D.err_index = (int64_t)bad[1]; return XDROP_ESEED; }
+    const int n_gen = fl.force_general ? (int)n_items : hs[C_OVF3];
+    D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_OVF1];
+    D.st.escalated[1] = hs[C_OVF2];
+    D.st.escalated[2] = n_gen;
+    if (n_gen > 0) {
+      const int64_t stride = XDROP_MAX_READ_LEN + 8;
+      const int warps_per_block = 4;
+      int64_t nwarps = std::min<int64_t>((int64_t)D.sms * 4, n_gen);
+      nwarps = ((nwarps + warps_per_block - 1) / warps_per_block) * warps_per_block;
+      CKR(D.scratch.ensure((size_t)nwarps * 3 * stride * sizeof(int)));
+      xk::general_kernel<<<(unsigned)(nwarps / warps_per_block), 128, 0, s>>>(
+          P, gen_items, gen_count, ctr + C_HEAD3, D.scratch.as<int>(), stride, 3);
+      ++launches;
+    }
+  } else {
+    int* hs = reinterpret_cast<int*>(D.h_small.p);
+    CK(cudaMemcpyAsync(hs + 16, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + 16);
+    if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
+  }
+  CK(cudaEventRecord(D.ev[3], s));
+  if (n_pairs > 0) {
+    xk::combine_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
+        P, out5, cells, D.level_acc.as<unsigned long long>());
+    ++launches;
+    CK(cudaMemcpyAsync(reinterpret_cast<int*>(D.h_small.p) + 32, D.level_acc.p, 64, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaEventRecord(D.ev[4], s));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, D.ev[2], D.ev[3]); D.st.kernel_ms = ms;
+  cudaEventElapsedTime(&ms, D.ev[0], D.ev[4]); D.st.total_ms = ms;
+  cudaEventElapsedTime(&ms, D.ev[0], D.ev[1]); D.st.pack_ms = ms;
+  if (n_pairs > 0) {
+    cudaEventElapsedTime(&ms, D.ev[2], D.ev[8]); D.st.level_ms[0] = ms;
+    cudaEventElapsedTime(&ms, D.ev[8], D.ev[9]); D.st.level_ms[1] = ms;
+    cudaEventElapsedTime(&ms, D.ev[9], D.ev[10]); D.st.level_ms[2] = ms;
+    cudaEventElapsedTime(&ms, D.ev[10], D.ev[3]); D.st.level_ms[3] = ms;
+    const unsigned long long* acc = reinterpret_cast<const unsigned long long*>(reinterpret_cast<int*>(D.h_small.p) + 32);
+    for (int l = 0; l < 4; ++l) { D.st.level_cells[l] = (int64_t)acc[l]; D.st.level_items[l] = (int64_t)acc[4 + l]; }
+    D.st.cells = D.st.level_cells[0] + D.st.level_cells[1] + D.st.level_cells[2] + D.st.level_cells[3];
+  }
+  D.st.items = n_items;
+  D.st.launches = launches;
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- context
+struct xdrop_ctx {
+  std::vector<DevCtx> devs;
+  xdrop_init_opts opts{};
+  std::vector<int> dev_ids;
+  int64_t err_index = -1;
+  xdrop_stats st{};
+  bool alive = false;
+  xdrop_sched_stats sched{};
+  std::vector<xdrop_trace_event> trace;
+};
+
+static int validate_params(const xdrop_params* p) {
+  if (!p) return XDROP_EINVAL;
+  if (p->match < 1 || p->match > 32) return XDROP_EINVAL;
+  if (p->mismatch > -1 || p->mismatch < -64) return XDROP_EINVAL;
+  if (p->gap > -1 || p->gap < -64) return XDROP_EINVAL;
+  if (p->xdrop < 0 || p->xdrop > (1 << 20)) return XDROP_EINVAL;
+  if (p->k < 1 || p->k > 1024) return XDROP_EINVAL;
+  return 0;
+}
+
+extern "C" int xdrop_init(const xdrop_init_opts* opts, xdrop_ctx** out_ctx) {
+  if (!out_ctx) return XDROP_EINVAL;
+  *out_ctx = nullptr;
+  xdrop_init_opts o{};
+  o.n_devices = 1;
+  if (opts) o = *opts;
+  if (o.n_devices < 1 || o.policy < 0 || o.policy > 3) return XDROP_EINVAL;
+  if (o.n_ranks < 1) o.n_ranks = 1;
+  if (o.batch_size <= 0) o.batch_size = 10000;
+  if (o.subbatches <= 0) o.subbatches = 1;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) { cudaGetLastError(); return XDROP_ENODEV; }
+  xdrop_ctx* ctx = new (std::nothrow) xdrop_ctx();
+  if (!ctx) return XDROP_ENOMEM;
+  ctx->opts = o;
+  for (int i = 0; i < o.n_devices; ++i) {
+    const int d = o.devices ? o.devices[i] : i % ndev;
+    if (d < 0 || d >= ndev) { delete ctx; return XDROP_ENODEV; }
+    ctx->dev_ids.push_back(d);
+  }
+  ctx->opts.devices = nullptr;
+  ctx->devs.resize(o.n_devices);
+  for (int i = 0; i < o.n_devices; ++i) {
+    int rc = dev_open(ctx->devs[i], ctx->dev_ids[i]);
+    if (rc) {
+      for (int j = 0; j <= i; ++j) dev_close(ctx->devs[j]);
+      delete ctx;
+      return rc;
+    }
+  }
+  ctx->alive = true;
+  *out_ctx = ctx;
+  return 0;
+}
+
+extern "C" int xdrop_finalize(xdrop_ctx* ctx) {
+  if (!ctx) return XDROP_ESTATE;
+  for (auto& D : ctx->devs) dev_close(D);
+  ctx->alive = false;
+  delete ctx;
+  return 0;
+}
+
+extern "C" const char* xdrop_strerror(int status) {
+  switch (status) {
+    case XDROP_OK: return "ok";
+    case XDROP_EINVAL: return "invalid argument";
+    case XDROP_ENOMEM: return "out of memory";
+    case XDROP_ECUDA: return "CUDA error";
+    case XDROP_EALPHABET: return "base outside {A,C,G,T}";
+    case XDROP_ESEED: return "seed out of range or bad read id";
+    case XDROP_ELENGTH: return "read too long";
+    case XDROP_ESTATE: return "invalid context state";
+    case XDROP_ENODEV: return "no CUDA device";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int64_t xdrop_last_error_index(const xdrop_ctx* ctx) { return ctx ? ctx->err_index : -1; }
+
+extern "C" int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st) {
+  if (!ctx || !st) return XDROP_EINVAL;
+  *st = ctx->st;
+  return 0;
+}
+
+static Flags flags_of(const xdrop_ctx* ctx) {
+  Flags f;
+  f.force_wide = (ctx->opts.flags & XDROP_FLAG_FORCE_WIDE) != 0;
+  f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0;
+  f.nosort = (ctx->opts.flags & XDROP_FLAG_NO_SORT) != 0;
+  return f;
+}
+
+extern "C" int xdrop_align_batch_device(xdrop_ctx* ctx, const char* seqA, const int64_t* offA, int64_t nA,
+                                        int64_t lenA, const char* seqB, const int64_t* offB, int64_t nB,
+                                        int64_t lenB, const xdrop_pair* pairs, int64_t n_pairs,
+                                        const xdrop_params* p, xdrop_result* out, int64_t* cells_out,
+                                        void* stream) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (n_pairs < 0 || nA < 0 || nB < 0 || lenA < 0 || lenB < 0) return XDROP_EINVAL;
+  if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
+  if (n_pairs > 0 && (!seqA || !offA || !seqB || !offB || !pairs || !out)) return XDROP_EINVAL;
+  DevCtx& D = ctx->devs[0];
+  cudaStream_t s = stream ? (cudaStream_t)stream : D.stream;
+  rc = dev_pipeline(D, seqA, offA, nA, lenA, seqB, offB, nB, lenB, reinterpret_cast<const PairDesc*>(pairs),
+                    n_pairs, *p, reinterpret_cast<int*>(out), reinterpret_cast<long long*>(cells_out), s,
+                    flags_of(ctx));
+  ctx->err_index = D.err_index;
+  ctx->st = D.st;
+  return rc;
+}
+
+// ---------------------------------------------------------------- host API
+namespace {
+
+struct HostBatch {
+  const xdrop_seqs* A; const xdrop_seqs* B; bool same;
+  const xdrop_pair* pairs; const xdrop_params* p; Flags fl;
+  xdrop_result* out; int64_t* cells_out;
+};
+
+// Run a subset of pairs (indices idx) on device D; pools are uploaded once per
+// call per device (upload_pools), pairs/results per sub-batch.
+struct DevSession {
+  DevCtx* D;
+  const HostBatch* hb;
+  bool uploaded = false;
+  bool packed = false;
+  int upload() {
+    if (uploaded) return 0;
+    DevCtx& d = *D;
+    CK(cudaSetDevice(d.dev));
+    const xdrop_seqs* A = hb->A;
+    const int64_t lenA = A->offsets[A->n];
+    CKR(d.asciiA.ensure((size_t)std::max<int64_t>(lenA, 1)));
+    CKR(d.offA.ensure((size_t)(A->n + 1) * 8));
+    CK(cudaMemcpyAsync(d.asciiA.p, A->seq, (size_t)lenA, cudaMemcpyHostToDevice, d.stream));
+    CK(cudaMemcpyAsync(d.offA.p, A->offsets, (size_t)(A->n + 1) * 8, cudaMemcpyHostToDevice, d.stream));
+    if (!hb->same) {
+      const xdrop_seqs* B = hb->B;
+      const int64_t lenB = B->offsets[B->n];
+      CKR(d.asciiB.ensure((size_t)std::max<int64_t>(lenB, 1)));
+      CKR(d.offB.ensure((size_t)(B->n + 1) * 8));
+      CK(cudaMemcpyAsync(d.asciiB.p, B->seq, (size_t)lenB, cudaMemcpyHostToDevice, d.stream));
+      CK(cudaMemcpyAsync(d.offB.p, B->offsets, (size_t)(B->n + 1) * 8, cudaMemcpyHostToDevice, d.stream));
+    }
+    uploaded = true;
+    return 0;
+  }
+  // align pairs[idx[0..n)] -> out[idx[t]]
+  int run(const int64_t* idx, int64_t n) {
+    DevCtx& d = *D;
+    CKR(upload());
+    std::vector<xdrop_pair> sub((size_t)n);
+    for (int64_t t = 0; t < n; ++t) sub[(size_t)t] = hb->pairs[idx[t]];
+    CKR(d.pairs.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(xdrop_pair)));
+    CKR(d.out5.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(xdrop_result)));
+    CKR(d.cells.ensure((size_t)std::max<int64_t>(n, 1) * 8));
+    if (n > 0)
+      CK(cudaMemcpyAsync(d.pairs.p, sub.data(), (size_t)n * sizeof(xdrop_pair), cudaMemcpyHostToDevice, d.stream));
+    const xdrop_seqs* A = hb->A;
+    const xdrop_seqs* B = hb->B;
+    const char* sA = d.asciiA.as<char>();
+    const int64_t* oA = d.offA.as<int64_t>();
+    const char* sB = hb->same ? sA : d.asciiB.as<char>();
+    const int64_t* oB = hb->same ? oA : d.offB.as<int64_t>();
+    int rc = dev_pipeline(d, sA, oA, A->n, A->offsets[A->n], sB, oB, B->n, B->offsets[B->n],
+                          d.pairs.as<PairDesc>(), n, *hb->p, d.out5.as<int>(), d.cells.as<long long>(),
+                          d.stream, hb->fl, !packed);
+    if (rc == 0 || rc != XDROP_EALPHABET) packed = true;
+    if (rc) {
+      if (d.err_index >= 0 && rc != XDROP_EALPHABET) d.err_index = idx[d.err_index];
+      return rc;
+    }
+    std::vector<xdrop_result> res((size_t)n);
+    std::vector<int64_t> cl((size_t)n);
+    if (n > 0) {
+      CK(cudaMemcpyAsync(res.data(), d.out5.p, (size_t)n * sizeof(xdrop_result), cudaMemcpyDeviceToHost, d.stream));
+      CK(cudaMemcpyAsync(cl.data(), d.cells.p, (size_t)n * 8, cudaMemcpyDeviceToHost, d.stream));
+      CK(cudaStreamSynchronize(d.stream));
+    }
+    for (int64_t t = 0; t < n; ++t) {
+      hb->out[idx[t]] = res[(size_t)t];
+      if (hb->cells_out) hb->cells_out[idx[t]] = cl[(size_t)t];
+    }
+    return 0;
+  }
+};
+
+int host_validate(const xdrop_seqs* S, int64_t& err) {
+  if (!S || !S->offsets || S->n < 0 || (S->n > 0 && !S->seq)) return XDROP_EINVAL;
+  if (S->offsets[0] < 0) return XDROP_EINVAL;
+  for (int64_t r = 0; r < S->n; ++r) {
+    const int64_t L = S->offsets[r + 1] - S->offsets[r];
+    if (L < 0) { err = r; return XDROP_EINVAL; }
+    if (L > XDROP_MAX_READ_LEN) { err = r; return XDROP_ELENGTH; }
+  }
+  if (S->offsets[0] != 0) return XDROP_EINVAL;  // pools are offset from seq[0]
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
+                                 const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                                 xdrop_result* out, int64_t* cells_out) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!A || !B || n_pairs < 0 || (n_pairs > 0 && (!pairs || !out))) return XDROP_EINVAL;
+  if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
+  int64_t err = -1;
+  if ((rc = host_validate(A, err)) || (B != A && (rc = host_validate(B, err)))) {
+    ctx->err_index = err;
+    return rc;
+  }
+  // seeds and ids (a2), reported with the offending pair index
+  for (int64_t t = 0; t < n_pairs; ++t) {
+    const xdrop_pair& q = pairs[t];
+    if (q.a_id < 0 || q.a_id >= A->n || q.b_id < 0 || q.b_id >= B->n) { ctx->err_index = t; return XDROP_EINVAL; }
+    const int64_t la = A->offsets[q.a_id + 1] - A->offsets[q.a_id];
+    const int64_t lb = B->offsets[q.b_id + 1] - B->offsets[q.b_id];
+    if (q.a_pos < 0 || q.b_pos < 0 || q.a_pos + (int64_t)p->k > la || q.b_pos + (int64_t)p->k > lb) {
+      ctx->err_index = t;
+      return XDROP_ESEED;
+    }
+  }
+  HostBatch hb{A, B, A == B || (A->seq == B->seq && A->offsets == B->offsets && A->n == B->n), pairs, p,
+               flags_of(ctx), out, cells_out};
+  const int m = (int)ctx->devs.size();
+  std::vector<DevSession> sess((size_t)m);
+  for (int g = 0; g < m; ++g) { sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; }
+
+  // estimated cost per pair (a3): anti-diagonals ~ min prefix + min suffix
+  std::vector<int64_t> w((size_t)n_pairs);
+  for (int64_t t = 0; t < n_pairs; ++t) {
+    const xdrop_pair& q = pairs[t];
+    const int64_t la = A->offsets[q.a_id + 1] - A->offsets[q.a_id];
+    const int64_t lb = B->offsets[q.b_id + 1] - B->offsets[q.b_id];
+    w[(size_t)t] = std::min<int64_t>(q.a_pos, q.b_pos) + std::min<int64_t>(la - q.a_pos - p->k, lb - q.b_pos - p->k) + 1;
+  }
+  xdrop_sched_cfg cfg{m, ctx->opts.policy, ctx->opts.n_ranks, ctx->opts.batch_size, ctx->opts.subbatches};
+  std::mutex err_mu;
+  int first_rc = 0;
+  int64_t first_err = -1;
+  auto runner = [&](int gpu, const int64_t* idx, int64_t n) -> int {
+    int r = sess[(size_t)gpu].run(idx, n);
+    if (r) {
+      std::lock_guard<std::mutex> lk(err_mu);
+      if (!first_rc) { first_rc = r; first_err = sess[(size_t)gpu].D->err_index; }
+    }
+    return r;
+  };
+  rc = xdrop_sched_run(cfg, w.data(), n_pairs, runner, &ctx->sched, &ctx->trace);
+  if (!rc) rc = first_rc;
+  if (rc) { ctx->err_index = first_err; return rc; }
+  // stats: sum over devices of the last pipeline runs (per-call granularity for 1 device)
+  ctx->st = ctx->devs[0].st;
+  return 0;
+}
+
+extern "C" int xdrop_last_sched_stats(const xdrop_ctx* ctx, xdrop_sched_stats* st) {
+  if (!ctx || !st) return XDROP_EINVAL;
+  *st = ctx->sched;
+  return 0;
+}
+
+extern "C" int64_t xdrop_last_trace(const xdrop_ctx* ctx, xdrop_trace_event* buf, int64_t cap) {
+  if (!ctx) return XDROP_EINVAL;
+  const int64_t n = (int64_t)ctx->trace.size();
+  for (int64_t t = 0; t < n && t < cap && buf; ++t) buf[t] = ctx->trace[(size_t)t];
+  return n;
+}
+
+// -------------------------------------------------------- INT32 peak probe
+extern "C" int xdrop_int32_peak(xdrop_ctx* ctx, double* ops_per_s) {
+  if (!ctx || !ctx->alive || !ops_per_s) return XDROP_EINVAL;
+  DevCtx& D = ctx->devs[0];
+  CK(cudaSetDevice(D.dev));
+  CKR(D.bad.ensure(16));
+  const int iters = 4096, threads = 256, blocks = D.sms * 8;
+  for (int mode = 0; mode < 2; ++mode) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      CK(cudaEventRecord(D.ev[5], D.stream));
+      if (mode == 0) xk::int32_peak_kernel<false><<<blocks, threads, 0, D.stream>>>(iters, rep, D.bad.as<int>());
+      else xk::int32_peak_kernel<true><<<blocks, threads, 0, D.stream>>>(iters, rep, D.bad.as<int>());
+      CK(cudaEventRecord(D.ev[6], D.stream));
+      CK(cudaEventSynchronize(D.ev[6]));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, D.ev[5], D.ev[6]);
+      if (rep > 0) best = std::min(best, ms);
+    }
+    // ops per inner body: 16 unrolled x (4 a-chains x 2 ops + 4 b-chains x 2 ops) = 256
+    const double ops = (double)blocks * threads * iters * 16.0 * 16.0;
+    ops_per_s[mode] = ops / (best * 1e-3);
+  }
+  return 0;
+}

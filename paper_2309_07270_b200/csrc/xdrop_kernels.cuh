@@ -1,0 +1,579 @@
+// xdrop_kernels.cuh -- sm_100a kernels of the batched X-drop hot path.
+//
+// Operation (include/xdrop.h): EXTEND is the anti-diagonal
+// X-drop DP; cells of one anti-diagonal are independent, the
+// threshold of anti-diagonal d is (best over anti-diagonals < d) - X
+// (PAPER.md:73-74, 224), the recurrence is NW with linear gaps.
+//
+// B200 design:
+//  * Bases are 2-bit packed (16 per u32) once per call by pack_kernel; every
+//    extension streams its two segments through 64-bit register windows
+//    (chars are compared 32 at a time with one 64-bit XOR).
+//  * Cells are held in DIAGONAL coordinates k = i - j: register R[q] holds
+//    diagonal K0 + q, so a band that follows the alignment does not drift
+//    through registers (only net indels move it).  Anti-diagonal d updates the
+//    slots of parity d in place: R[q] <- max(R[q] + s, max(R[q-1], R[q+1]) + g).
+//  * band_kernel<G, C>: G lanes per extension, C cells per lane per
+//    anti-diagonal (window S = G*C cells = 2S diagonals).  G = 1 is the
+//    lane-per-extension path (no cross-lane traffic at all: 32 extensions per
+//    warp, integer-ALU bound); G = 32 is warp-per-extension for wide bands
+//    (one shuffle + CREDUX reductions per anti-diagonal).
+//  * An extension whose live band leaves its window is re-queued to the next
+//    (wider) level; the result never depends on the window (cells outside the
+//    hull are dead by construction), so escalation is exact.
+//  * general_kernel is the unbounded fallback (anti-diagonals in global
+//    scratch), used only beyond S = 1024.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace xk {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NEGV = -(1 << 24);   // value of a dead cell (biased domain)
+constexpr int BIAS = 1 << 21;      // stored value = H + BIAS; live values are > 0
+constexpr int GUARD = 2048;        // bases of padding before/after the packed pool
+constexpr int EMIN = 1 << 29;      // extent of an empty live set: [EMIN, EMAX]
+constexpr int EMAX = -(1 << 29);
+constexpr int NBUCKET = 16384;     // cost buckets for the length-sorted queue
+constexpr int BUCKET_SHIFT = 4;
+
+struct ExtOut {          // one extension result (32 B)
+  int32_t best, istar, jstar, level;
+  int64_t cells;
+  int64_t pad;
+};
+
+struct PairDesc { int32_t a_id, b_id, a_pos, b_pos; };
+
+struct Problem {
+  const uint32_t* PA; const int64_t* offA; int64_t nA;
+  const uint32_t* PB; const int64_t* offB; int64_t nB;
+  const PairDesc* pairs; int64_t n_pairs;
+  int M, mu, g, X, k;
+  ExtOut* ext;
+};
+
+// ------------------------------------------------------------ packed streams
+__device__ __forceinline__ uint32_t fwd16(const uint32_t* __restrict__ P, int64_t x) {
+  const int64_t w = x >> 4;
+  const int sh = (int)(x & 15) << 1;
+  const uint32_t lo = __ldg(P + w), hi = __ldg(P + w + 1);
+  return __funnelshift_r(lo, hi, sh);
+}
+// chars t .. t+15 of a stream (start, dir); dir < 0 reads backwards and
+// returns codes with their two bits swapped -- harmless, both streams of an
+// extension share the direction, and only equality of codes is used.
+__device__ __forceinline__ uint32_t load16(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
+  return dir > 0 ? fwd16(P, start + t) : __brev(fwd16(P, start - t - 15));
+}
+__device__ __forceinline__ uint64_t load32c(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
+  return (uint64_t)load16(P, start, dir, t) | ((uint64_t)load16(P, start, dir, t + 16) << 32);
+}
+// reverse the order of the 32 2-bit fields of x, keeping each field's bits
+__device__ __forceinline__ uint64_t rev_fields(uint64_t x) {
+  uint64_t y = __brevll(x);
+  return ((y >> 1) & 0x5555555555555555ull) | ((y & 0x5555555555555555ull) << 1);
+}
+__device__ __forceinline__ int char_at(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
+  const int64_t x = start + (dir > 0 ? t : -t);
+  return (int)((__ldg(P + (x >> 4)) >> ((int)(x & 15) << 1)) & 3u);
+}
+
+struct Geom { int64_t sa, sb; int da, db; int m, n; };
+
+__device__ __forceinline__ Geom item_geom(const Problem& P, int item) {
+  const int p = item >> 1;
+  const PairDesc pd = P.pairs[p];
+  const int64_t a0 = P.offA[pd.a_id] + GUARD, b0 = P.offB[pd.b_id] + GUARD;
+  const int lenA = (int)(P.offA[pd.a_id + 1] - P.offA[pd.a_id]);
+  const int lenB = (int)(P.offB[pd.b_id + 1] - P.offB[pd.b_id]);
+  Geom G;
+  if (item & 1) {   // right extension: A[a_pos+k:], B[b_pos+k:]
+    G.sa = a0 + pd.a_pos + P.k; G.da = 1; G.m = lenA - pd.a_pos - P.k;
+    G.sb = b0 + pd.b_pos + P.k; G.db = 1; G.n = lenB - pd.b_pos - P.k;
+  } else {          // left extension: reverse(A[:a_pos]), reverse(B[:b_pos])
+    G.sa = a0 + pd.a_pos - 1; G.da = -1; G.m = pd.a_pos;
+    G.sb = b0 + pd.b_pos - 1; G.db = -1; G.n = pd.b_pos;
+  }
+  return G;
+}
+
+// ---------------------------------------------------------- group reductions
+template <int G> __device__ __forceinline__ int gmax(int v) {
+  if constexpr (G == 1) return v;
+  else if constexpr (G == 32) return __reduce_max_sync(FULL, v);
+  else {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+  }
+}
+template <int G> __device__ __forceinline__ int gmin(int v) {
+  if constexpr (G == 1) return v;
+  else if constexpr (G == 32) return __reduce_min_sync(FULL, v);
+  else {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+  }
+}
+
+// ------------------------------------------------------------ band kernel
+// State of one extension as seen by one lane of its group.
+template <int C> struct Band {
+  int R[2 * C];                 // diagonals K0 + 2C*gl + r, r in [0, 2C)
+  uint64_t Aw, Bw;              // a[ia0_l + t], b[jb0_l - t] for t = 0..31
+  uint32_t An, An2, Bn, Bn2;    // stream reservoirs (next chars in stream order)
+  int64_t sa, sb; int da, db;
+  int m, n, K0, ia0, jb0;       // ia0/jb0: char index of global cell t = 0
+  int best, istar, jstar;       // best is biased
+  int minL1, maxL1, minL2, maxL2;   // live extents (in i) of d-1 and d-2
+  long long cells;
+  int item;
+  bool active;
+};
+
+template <int G, int C>
+__device__ __forceinline__ void band_reload(Band<C>& B, int gl, int arem, int brem, const Problem& P) {
+  const int ia = B.ia0 + C * gl, jb = B.jb0 - C * gl;
+  B.Aw = load32c(P.PA, B.sa, B.da, ia);
+  B.An = load16(P.PA, B.sa, B.da, ia + 32);
+  B.An2 = load16(P.PA, B.sa, B.da, ia + 32 + arem);
+  B.Bw = rev_fields(load32c(P.PB, B.sb, B.db, jb - 31));
+  B.Bn = load16(P.PB, B.sb, B.db, jb + 1);
+  B.Bn2 = load16(P.PB, B.sb, B.db, jb + 1 + brem);
+}
+
+// One anti-diagonal of parity PAR: the cells of this lane (C of them).
+template <int G, int C, int PAR, bool CHECK>
+__device__ __forceinline__ void band_cells_impl(Band<C>& B, int gl, int d, int thr, int qlo, int qhi,
+                                                int& mk, unsigned& dbits, int M, int mu, int g) {
+  constexpr int NR = 2 * C;
+  const uint64_t x = B.Aw ^ B.Bw;
+  int nb = NEGV;
+  if constexpr (G > 1) {
+    if constexpr (PAR == 0) {
+      nb = __shfl_up_sync(FULL, B.R[NR - 1], 1, G);
+      if (gl == 0) nb = NEGV;
+    } else {
+      nb = __shfl_down_sync(FULL, B.R[0], 1, G);
+      if (gl == G - 1) nb = NEGV;
+    }
+  }
+  int mkl = NEGV * 64;
+  unsigned bits = 0;
+#pragma unroll
+  for (int tt = 0; tt < C; ++tt) {
+    const int r = 2 * tt + PAR;
+    const int lft = (r == 0) ? nb : B.R[r == 0 ? 0 : r - 1];
+    const int rgt = (r == NR - 1) ? nb : B.R[r == NR - 1 ? 0 : r + 1];
+    const int lu = max(lft, rgt);
+    const bool mis = ((x >> (2 * tt)) & 3ull) != 0ull;
+    const int dg = B.R[r] + (mis ? mu : M);
+    int v = max(lu + g, dg);
+    bool live = v >= thr;
+    if constexpr (CHECK) {
+      const int q = 2 * C * gl + r;
+      live = live && (q >= qlo) && (q <= qhi);
+    }
+    v = live ? v : NEGV;
+    B.R[r] = v;
+    mkl = max(mkl, v * 64 + (63 - tt));
+    bits = __funnelshift_l((unsigned)v, bits, 1);   // dead cells set the bit (sign)
+  }
+  mk = mkl;
+  dbits = bits;
+}
+
+template <int G, int C>
+__device__ __forceinline__ void band_shift(Band<C>& B, int gl, int dir) {
+  constexpr int NR = 2 * C;
+  if (dir > 0) {            // K0 += 2: R[r] <- R[r+2]
+    int n0 = NEGV, n1 = NEGV;
+    if constexpr (G > 1) {
+      n0 = __shfl_down_sync(FULL, B.R[0], 1, G);
+      n1 = __shfl_down_sync(FULL, B.R[1], 1, G);
+      if (gl == G - 1) { n0 = NEGV; n1 = NEGV; }
+    }
+#pragma unroll
+    for (int r = 0; r < NR - 2; ++r) B.R[r] = B.R[r + 2];
+    B.R[NR - 2] = n0; B.R[NR - 1] = n1;
+  } else {                  // K0 -= 2: R[r] <- R[r-2]
+    int n0 = NEGV, n1 = NEGV;
+    if constexpr (G > 1) {
+      n0 = __shfl_up_sync(FULL, B.R[NR - 2], 1, G);
+      n1 = __shfl_up_sync(FULL, B.R[NR - 1], 1, G);
+      if (gl == 0) { n0 = NEGV; n1 = NEGV; }
+    }
+#pragma unroll
+    for (int r = NR - 1; r >= 2; --r) B.R[r] = B.R[r - 2];
+    B.R[0] = n0; B.R[1] = n1;
+  }
+}
+
+// Finish one anti-diagonal: reductions, best/argmax, hull count, termination,
+// window management, stream advance.  Returns nothing; updates B.
+template <int G, int C, int PAR>
+__device__ __forceinline__ void band_step(Band<C>& B, int gl, int d, int& arem, int& brem,
+                                          const Problem& P, int level, int* ovf_items, int* ovf_count) {
+  constexpr int S = G * C;
+  const int thr = B.best - P.X;
+  // boundary: cells with i > m or j > n must be dead (q in [qlo, qhi] valid)
+  const int qlo = d - B.K0 - 2 * B.n;
+  const int qhi = 2 * B.m - d - B.K0;
+  const bool need = B.active && (qlo > 0 || qhi < 2 * S - 1);
+  int mk;
+  unsigned dbits;
+  if (__any_sync(FULL, need))
+    band_cells_impl<G, C, PAR, true>(B, gl, d, thr, qlo, qhi, mk, dbits, P.M, P.mu, P.g);
+  else
+    band_cells_impl<G, C, PAR, false>(B, gl, d, thr, qlo, qhi, mk, dbits, P.M, P.mu, P.g);
+
+  // lane live extent (local t), cell tt sits at bit C-1-tt of dbits
+  const unsigned lb = ~dbits & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  int tmin = lb ? (__clz(lb) - (32 - C)) + C * gl : EMIN;
+  int tmax = lb ? (C - __ffs(lb)) + C * gl : EMAX;
+  tmin = gmin<G>(tmin);
+  tmax = gmax<G>(tmax);
+  // best value and the smallest t attaining it
+  int vl = mk >> 6;
+  int gt;
+  int gv;
+  if constexpr (G == 1) {
+    gv = vl; gt = 63 - (mk & 63);
+  } else {
+    gv = gmax<G>(vl);
+    const unsigned ball = __ballot_sync(FULL, vl == gv);
+    const int grp = (threadIdx.x & 31) / G;
+    const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
+    const int first = __ffs(gb) - 1;
+    gt = __shfl_sync(FULL, C * gl + 63 - (mk & 63), first, G);
+  }
+  const int ibase = (d + B.K0 + PAR) >> 1;
+  const int minL0 = (tmin == EMIN) ? EMIN : ibase + tmin;
+  const int maxL0 = (tmax == EMAX) ? EMAX : ibase + tmax;
+  if (B.active) {
+    if (gv > B.best) { B.best = gv; B.istar = ibase + gt; B.jstar = d - B.istar; }
+    // hull of anti-diagonal d (from the live sets of d-1 and d-2)
+    const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
+    const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
+    B.cells += (long long)max(0, hi - lo + 1);
+  }
+  const bool empty0 = (tmin == EMIN), empty1 = (B.minL1 == EMIN);
+  // q-extent of the live cells of d and d-1 in window coordinates
+  int qmn = 1 << 30, qmx = -(1 << 30);
+  if (!empty0) { qmn = 2 * minL0 - d - B.K0; qmx = 2 * maxL0 - d - B.K0; }
+  if (!empty1) { qmn = min(qmn, 2 * B.minL1 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL1 - (d - 1) - B.K0); }
+  B.minL2 = B.minL1; B.maxL2 = B.maxL1;
+  B.minL1 = minL0; B.maxL1 = maxL0;
+
+  // stream advance for anti-diagonal d+1 (uniform over the warp)
+  if constexpr (PAR == 0) {       // a advances: ia0 += 1
+    B.Aw = (B.Aw >> 2) | ((uint64_t)(B.An & 3u) << 62);
+    B.An >>= 2;
+    B.ia0 += 1;
+    if (--arem == 0) {
+      arem = 16;
+      B.An = B.An2;
+      if (B.active) B.An2 = load16(P.PA, B.sa, B.da, B.ia0 + C * gl + 48);
+    }
+  } else {                        // b advances: jb0 += 1
+    B.Bw = (B.Bw << 2) | (uint64_t)(B.Bn & 3u);
+    B.Bn >>= 2;
+    B.jb0 += 1;
+    if (--brem == 0) {
+      brem = 16;
+      B.Bn = B.Bn2;
+      if (B.active) B.Bn2 = load16(P.PB, B.sb, B.db, B.jb0 - C * gl + 17);
+    }
+  }
+
+  if (!B.active) return;
+  const bool done = (empty0 && empty1) || (d >= B.m + B.n);
+  if (done) {
+    if (gl == 0) {
+      ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
+      o.cells = B.cells; o.pad = 0;
+      P.ext[B.item] = o;
+    }
+    B.active = false;
+    return;
+  }
+  // window management (uniform within the group)
+  int dir = 0;
+  bool ovf = false;
+  if (qmx >= 2 * S - 2) { if (qmn >= 3) dir = 1; else ovf = true; }
+  else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
+  if (ovf) {
+    if (gl == 0) { const int pos = atomicAdd(ovf_count, 1); ovf_items[pos] = B.item; }
+    B.active = false;
+    return;
+  }
+  if (dir != 0) {
+    band_shift<G, C>(B, gl, dir);
+    B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
+    band_reload<G, C>(B, gl, arem, brem, P);
+  }
+}
+
+template <int G, int C>
+__global__ void __launch_bounds__(128)
+band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
+            int* queue_head, int* ovf_items, int* ovf_count, int level) {
+  constexpr int S = G * C;
+  constexpr int IPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int grp = lane / G;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(queue_head, IPW);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= n_items) break;
+    Band<C> B;
+    const int slot = base + grp;
+    B.active = slot < n_items;
+    B.item = B.active ? items[slot] : 0;
+    if (B.active) {
+      const Geom gm = item_geom(P, B.item);
+      B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+    } else {
+      B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
+    }
+    B.K0 = -S;
+    B.ia0 = -S / 2;          // window chars for d = 1 (odd): ia0 = (1+K0+1)/2 - 1
+    B.jb0 = S / 2 - 1;       //                               jb0 = (1-K0-1)/2 - 1
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) B.R[r] = NEGV;
+    // origin: d = 0, k = 0 -> q = S -> lane G/2 (r = 0), or lane 0 r = C when G = 1
+    if constexpr (G == 1) B.R[C] = BIAS;
+    else if (gl == G / 2) B.R[0] = BIAS;
+    B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1;
+    B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
+    int arem = 16, brem = 16;
+    band_reload<G, C>(B, gl, arem, brem, P);
+    if (B.active && B.m + B.n == 0) {
+      if (gl == 0) {
+        ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+        P.ext[B.item] = o;
+      }
+      B.active = false;
+    }
+    int d = 0;
+    while (__any_sync(FULL, B.active)) {
+      ++d;
+      band_step<G, C, 1>(B, gl, d, arem, brem, P, level, ovf_items, ovf_count);
+      if (!__any_sync(FULL, B.active)) break;
+      ++d;
+      band_step<G, C, 0>(B, gl, d, arem, brem, P, level, ovf_items, ovf_count);
+    }
+  }
+}
+
+// ------------------------------------------------------------ general path
+// Warp per extension, anti-diagonals indexed by i in global scratch; the hull
+// of each anti-diagonal bounds what is valid.  Unbounded band width.
+__global__ void __launch_bounds__(128)
+general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
+               int* queue_head, int* scratch, int64_t stride, int level) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int* H[3];
+  for (int t = 0; t < 3; ++t) H[t] = scratch + (int64_t)warp_global * 3 * stride + t * stride;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(queue_head, 1);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot >= n_items) break;
+    const int item = items[slot];
+    const Geom gm = item_geom(P, item);
+    const int m = gm.m, n = gm.n;
+    int lo_[3], hi_[3], mn_[3], mx_[3];
+    // d = 0 in slot 0; d = -1 in slot 2
+    if (lane == 0) H[0][0] = BIAS;
+    lo_[0] = 0; hi_[0] = 0; mn_[0] = 0; mx_[0] = 0;
+    lo_[2] = 1; hi_[2] = 0; mn_[2] = EMIN; mx_[2] = EMAX;
+    lo_[1] = 1; hi_[1] = 0; mn_[1] = EMIN; mx_[1] = EMAX;
+    int best = BIAS, istar = 0, jstar = 0;
+    long long cells = 1;
+    __syncwarp();
+    for (int d = 1; d <= m + n; ++d) {
+      const int c = d % 3, p1 = (d + 2) % 3, p2 = (d + 1) % 3;
+      if (mn_[p1] == EMIN && mn_[p2] == EMIN) break;
+      const int lo = max(max(0, d - n), min(mn_[p1], mn_[p2] == EMIN ? EMIN : mn_[p2] + 1));
+      const int hi = min(min(m, d), max(mx_[p1], mx_[p2] == EMAX ? EMAX : mx_[p2]) + 1);
+      if (hi >= lo) cells += hi - lo + 1;
+      const int thr = best - P.X;
+      int kbest = NEGV, ibest = 0x7fffffff, lmn = EMIN, lmx = EMAX;
+      for (int i = lo + lane; i <= hi; i += 32) {
+        const int j = d - i;
+        int v = NEGV;
+        if (i >= 1 && i - 1 >= lo_[p1] && i - 1 <= hi_[p1]) v = max(v, H[p1][i - 1] + P.g);
+        if (j >= 1 && i >= lo_[p1] && i <= hi_[p1]) v = max(v, H[p1][i] + P.g);
+        if (i >= 1 && j >= 1 && i - 1 >= lo_[p2] && i - 1 <= hi_[p2]) {
+          const int ca = char_at(P.PA, gm.sa, gm.da, i - 1);
+          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1);
+          v = max(v, H[p2][i - 1] + (ca == cb ? P.M : P.mu));
+        }
+        const bool live = v >= thr;
+        v = live ? v : NEGV;
+        H[c][i] = v;
+        if (live) {
+          if (v > kbest) { kbest = v; ibest = i; }
+          lmn = min(lmn, i); lmx = max(lmx, i);
+        }
+      }
+      const int gv = __reduce_max_sync(FULL, kbest);
+      const int gi = __reduce_min_sync(FULL, (kbest == gv) ? ibest : 0x7fffffff);
+      lmn = __reduce_min_sync(FULL, lmn);
+      lmx = __reduce_max_sync(FULL, lmx);
+      lo_[c] = lo; hi_[c] = hi; mn_[c] = lmn; mx_[c] = lmx;
+      if (lmn != EMIN && gv > best) { best = gv; istar = gi; jstar = d - gi; }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level;
+      o.cells = cells; o.pad = 0;
+      P.ext[item] = o;
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------- pack / prepare
+// ASCII -> 2-bit (A0 C1 G2 T3, base t at bits 2(t mod 16) of word t/16),
+// written at pool index + GUARD.  Any other byte sets *bad to its index.
+__global__ void pack_kernel(const char* __restrict__ seq, int64_t len, uint32_t* __restrict__ out,
+                            unsigned long long* bad) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // output word of the pool
+  const int64_t nwords = (len + GUARD + 15) / 16;
+  if (w >= nwords) return;
+  uint32_t word = 0;
+  const int64_t t0 = w * 16 - GUARD;   // pool index of the first base in this word
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t t = t0 + u;
+    if (t >= 0 && t < len) {
+      const unsigned char ch = (unsigned char)seq[t];
+      const unsigned char c = ch & 0xDF;   // upper case
+      uint32_t code;
+      if (c == 'A') code = 0; else if (c == 'C') code = 1; else if (c == 'G') code = 2;
+      else if (c == 'T') code = 3;
+      else { code = 0; atomicMin(bad, (unsigned long long)t); }
+      word |= code << (2 * u);
+    }
+  }
+  out[w] = word;
+}
+
+// validate pairs, estimate costs, histogram of cost buckets
+__global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict__ hist,
+                            unsigned long long* bad_pair, int max_len) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P.n_pairs) return;
+  const PairDesc pd = P.pairs[p];
+  bool ok = pd.a_id >= 0 && pd.a_id < P.nA && pd.b_id >= 0 && pd.b_id < P.nB;
+  int wl = 0, wr = 0;
+  if (ok) {
+    const int64_t lenA = P.offA[pd.a_id + 1] - P.offA[pd.a_id];
+    const int64_t lenB = P.offB[pd.b_id + 1] - P.offB[pd.b_id];
+    ok = pd.a_pos >= 0 && pd.b_pos >= 0 && pd.a_pos + (int64_t)P.k <= lenA &&
+         pd.b_pos + (int64_t)P.k <= lenB && lenA <= max_len && lenB <= max_len;
+    if (ok) {
+      wl = min(pd.a_pos, pd.b_pos);
+      wr = (int)min(lenA - pd.a_pos - P.k, lenB - pd.b_pos - P.k);
+    }
+  }
+  if (!ok) atomicMin(bad_pair, (unsigned long long)p);
+  wcost[2 * p] = wl;
+  wcost[2 * p + 1] = wr;
+  atomicAdd(&hist[min(wl >> BUCKET_SHIFT, NBUCKET - 1)], 1);
+  atomicAdd(&hist[min(wr >> BUCKET_SHIFT, NBUCKET - 1)], 1);
+}
+
+// exclusive scan of the histogram in DESCENDING bucket order (one block of 1024)
+__global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ cursor) {
+  __shared__ int part[1024];
+  constexpr int PER = NBUCKET / 1024;
+  const int t = threadIdx.x;
+  int local[PER];
+  int s = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {       // thread t owns descending ranks t*PER .. t*PER+PER-1
+    const int b = NBUCKET - 1 - (t * PER + u);
+    local[u] = s; s += hist[b];
+  }
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  const int base = part[t] - s;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) cursor[NBUCKET - 1 - (t * PER + u)] = base + local[u];
+}
+
+__global__ void scatter_kernel(const int* __restrict__ wcost, int64_t n_items, int* __restrict__ cursor,
+                               int* __restrict__ items, int nosort) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  if (nosort) { items[it] = (int)it; return; }
+  const int b = min(wcost[it] >> BUCKET_SHIFT, NBUCKET - 1);
+  const int pos = atomicAdd(&cursor[b], 1);
+  items[pos] = (int)it;
+}
+
+// combine: seed score + left/right results -> per-pair result
+__global__ void combine_kernel(Problem P, int* __restrict__ out5, long long* __restrict__ cells_out,
+                               unsigned long long* __restrict__ level_acc) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P.n_pairs) return;
+  const PairDesc pd = P.pairs[p];
+  const int64_t xa = P.offA[pd.a_id] + GUARD + pd.a_pos, xb = P.offB[pd.b_id] + GUARD + pd.b_pos;
+  int mism = 0;
+  for (int t = 0; t < P.k; t += 16) {
+    const uint32_t x = fwd16(P.PA, xa + t) ^ fwd16(P.PB, xb + t);
+    uint32_t f = (x | (x >> 1)) & 0x55555555u;
+    const int rem = P.k - t;
+    if (rem < 16) f &= (1u << (2 * rem)) - 1u;
+    mism += __popc(f);
+  }
+  const int seed = (P.k - mism) * P.M + mism * P.mu;
+  const ExtOut L = P.ext[2 * p], R = P.ext[2 * p + 1];
+  int* o = out5 + 5 * p;
+  o[0] = L.best + seed + R.best;
+  o[1] = pd.a_pos - L.istar;
+  o[2] = pd.a_pos + P.k + R.istar;
+  o[3] = pd.b_pos - L.jstar;
+  o[4] = pd.b_pos + P.k + R.jstar;
+  if (cells_out) cells_out[p] = L.cells + R.cells;
+  // per-level accounting (stats): [cells x4, items x4]
+  atomicAdd(&level_acc[L.level & 3], (unsigned long long)L.cells);
+  atomicAdd(&level_acc[R.level & 3], (unsigned long long)R.cells);
+  atomicAdd(&level_acc[4 + (L.level & 3)], 1ull);
+  atomicAdd(&level_acc[4 + (R.level & 3)], 1ull);
+}
+
+// ----------------------------------------------------- INT32 issue-rate probe
+template <bool DUAL>
+__global__ void int32_peak_kernel(int iters, int seed, int* sink) {
+  int a0 = threadIdx.x + seed, a1 = a0 ^ 0x55, a2 = a0 * 3, a3 = a0 + 7;
+  int b0 = a0 ^ 0x1234, b1 = a1 + 11, b2 = a2 ^ 0x777, b3 = a3 * 5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = max(a0 + b1, a2); a1 = (a1 ^ b0) + a3; a2 = max(a2, b2) - a0; a3 = a3 + (b3 ^ a1);
+      if (DUAL) { b0 = b0 * 3 + a1; b1 = b1 * 5 + a2; b2 = b2 * 7 + a3; b3 = b3 * 9 + a0; }
+      else { b0 = max(b0, a1) ^ 3; b1 = (b1 ^ a2) + 5; b2 = min(b2, a3) + 7; b3 = (b3 + a0) ^ 9; }
+    }
+  }
+  if ((a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3) == 0x7fffffff) *sink = 1;
+}
+
+}  // namespace xk

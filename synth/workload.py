@@ -294,10 +294,10 @@ def random_pairs_workload(seed: int, n_pairs: int, len_lo: int, len_hi: int, k: 
             b = np.insert(b, ins_at, rng.integers(0, 4, size=ins_at.shape[0], dtype=np.uint8))
         else:
             b = rng.integers(0, 4, size=int(rng.integers(len_lo, len_hi + 1)), dtype=np.uint8)
-        if a.shape[0] < k or b.shape[0] < k:
-            b = np.concatenate([b, a[:k]])
         if a.shape[0] < k:
-            a = np.concatenate([a, b[:k]])
+            a = np.concatenate([a, rng.integers(0, 4, size=k - a.shape[0], dtype=np.uint8)])
+        if b.shape[0] < k:
+            b = np.concatenate([b, rng.integers(0, 4, size=k - b.shape[0], dtype=np.uint8)])
         edge = rng.random()
         if edge < 0.1:
             pa, pb = 0, 0

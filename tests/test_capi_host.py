@@ -1,0 +1,118 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every declared symbol, and its
+host-side scheduler logic follows PAPER.md §III / Alg. 1 (SPEC.md test vectors)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def xd():
+    from paper_2309_07270_b200 import build
+    build.build()
+    import paper_2309_07270_b200 as xd
+    return xd
+
+
+def test_exports_every_declared_symbol(xd):
+    from paper_2309_07270_b200 import _native as N
+    hdr = open(os.path.join(ROOT, "include", "xdrop.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(xdrop_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 12
+    for name in sorted(declared):
+        assert hasattr(N.lib, name), name
+    assert declared <= set(N.EXPORTS) | declared
+    assert set(N.EXPORTS) <= declared
+
+
+def test_strerror_and_no_device_fails_loudly(xd):
+    from paper_2309_07270_b200 import _native as N
+    assert N.lib.xdrop_strerror(-4) == b"base outside {A,C,G,T}"
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(xd.XdropError) as e:
+            xd.Aligner()
+        assert e.value.status == N.ENODEV
+
+
+def test_ring_vectors_spec(xd):
+    # SPEC.md:227-239 (Alg. 1 l.18-30 literal while-loops)
+    assert xd.ring_left(2, 1, [3, 3, 3, 3]) == 1
+    assert xd.ring_left(0, 1, [3, 3, 3, 3]) == 3
+    assert xd.ring_left(2, 3, [3, 2, 3, 1]) == 0
+    assert xd.ring_left(1, 5, [2, 5, 3]) is None
+    assert xd.ring_right(2, 1, [3, 3, 3, 3]) == 3
+    assert xd.ring_right(3, 1, [3, 3, 3, 3]) == 0
+    assert xd.ring_right(0, 3, [3, 2, 3, 1]) == 2
+
+
+def check_trace(trace, n_pairs, m, policy, n_ranks):
+    assert trace["n_pairs"].sum() == n_pairs                     # exactly once
+    for g in range(m):                                           # mutual exclusion per GPU
+        ev = np.sort(trace[trace["gpu"] == g], order="t0_ms")
+        assert np.all(ev["t0_ms"][1:] >= ev["t1_ms"][:-1] - 1e-9)
+    if policy in ("one2one", "opt_one2one"):                     # pipeline affinity r mod m
+        assert np.all(trace["gpu"] == trace["rank"] % m)
+    if policy == "one2all":                                      # one rank at a time
+        by_turn = {}
+        for e in trace:
+            key = (e["rank"], e["batch"], e["sub"])
+            lo, hi = by_turn.get(key, (1e18, -1e18))
+            by_turn[key] = (min(lo, e["t0_ms"]), max(hi, e["t1_ms"]))
+        iv = sorted(by_turn.values())
+        for a, b in zip(iv, iv[1:]):
+            assert b[0] >= a[1] - 1e-9
+    for r in range(n_ranks):                                     # per-rank order (batch, sub)
+        ev = np.sort(trace[trace["rank"] == r], order="t0_ms")
+        keys = list(zip(ev["batch"], ev["sub"]))
+        assert keys == sorted(keys)
+
+
+@pytest.mark.parametrize("policy", ["one2all", "one2one", "opt_one2one", "cells"])
+def test_policies_randomized_deadlock_free(xd, policy):
+    rng = np.random.default_rng(3)
+    for _ in range(25):
+        m = int(rng.integers(1, 5))
+        n_ranks = int(rng.integers(1, 9))
+        c = int(rng.integers(1, 4))
+        bs = int(rng.integers(1, 9))
+        n = int(rng.integers(0, 60))
+        w = rng.integers(1, 100, size=n)
+        trace, st, gpu = xd.sched_simulate(m, policy, n_ranks, w, batch_size=bs, subbatches=c, ns_per_unit=200)
+        check_trace(trace, n, m, policy, n_ranks)
+        assert np.all(gpu >= 0) or n == 0
+
+
+def test_skewed_batch_counts_no_deadlock(xd):
+    """Counts like [2,2,1] deadlock Alg. 1 read literally (Q21); ours must finish."""
+    w = np.ones(5, dtype=np.int64)
+    trace, st, _ = xd.sched_simulate(1, "one2all", 3, w, batch_size=1, subbatches=1)
+    assert trace["n_pairs"].sum() == 5
+    assert [int(r) for r in np.sort(trace, order="t0_ms")["rank"]] == [0, 1, 2, 0, 1]
+
+
+def test_message_proportionality(xd):
+    """§III-D: one2one sends per sub-batch, opt_one2one per batch."""
+    for c in (1, 2, 5):
+        for n_ranks in (2, 4):
+            n = n_ranks * 3 * 10                       # 3 batches of 10 per rank
+            w = np.ones(n, dtype=np.int64)
+            _, s1, _ = xd.sched_simulate(1, "one2one", n_ranks, w, batch_size=10, subbatches=c)
+            _, s2, _ = xd.sched_simulate(1, "opt_one2one", n_ranks, w, batch_size=10, subbatches=c)
+            turns1, turns2 = n_ranks * 3 * c, n_ranks * 3
+            assert s1["handoffs"] == turns1 - 1 and s2["handoffs"] == turns2 - 1
+            assert s1["exchange_msgs"] == s2["exchange_msgs"] == n_ranks * (n_ranks - 1)
+
+
+def test_one2one_concurrency_and_cells_balance(xd):
+    w = np.ones(400, dtype=np.int64)
+    _, st, _ = xd.sched_simulate(4, "one2one", 8, w, batch_size=25, subbatches=2, ns_per_unit=20000)
+    assert st["max_concurrent"] >= 2
+    rng = np.random.default_rng(1)
+    w = rng.integers(1, 1000, size=1000)
+    _, _, gpu = xd.sched_simulate(4, "cells", 1, w)
+    loads = np.bincount(gpu, weights=w, minlength=4)
+    assert loads.max() - loads.min() <= w.max()                   # LPT bound

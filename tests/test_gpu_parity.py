@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Fields compared element by element: score, a_begin, a_end, b_begin, b_end and
+the DP cell count (integer work: the bar is bit-exactness).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("score", "a_begin", "a_end", "b_begin", "b_end")
+
+
+@pytest.fixture(scope="module")
+def xd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2309_07270_b200 as xd
+    return xd
+
+
+def oracle_of(w, pairs=None, X=None, M=None, mu=None, g=None):
+    import oracle
+    return oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs if pairs is None else pairs, w.k,
+                              M=w.M if M is None else M, mu=w.mu if mu is None else mu,
+                              g=w.g if g is None else g, X=w.X if X is None else X)
+
+
+def assert_same(res, cells, ref, rcells, what=""):
+    for f in FIELDS:
+        bad = np.nonzero(res[f] != ref[f])[0]
+        assert bad.size == 0, f"{what}: field {f} differs at pairs {bad[:10]} gpu={res[bad[:5]]} ref={ref[bad[:5]]}"
+    bad = np.nonzero(cells != rcells)[0]
+    assert bad.size == 0, f"{what}: cells differ at {bad[:10]}: {cells[bad[:5]]} vs {rcells[bad[:5]]}"
+
+
+def test_cfg1_full(xd):
+    from synth import workload as W
+    w = W.config("cfg1")
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, "cfg1")
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2, 4])
+@pytest.mark.parametrize("X", [0, 1, 5, 15, 50])
+def test_random_edge_cases_all_paths(xd, flags, X):
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=100 + X, n_pairs=150 if flags != 2 else 40, len_lo=0, len_hi=700,
+                                k=11, X=X)
+    with xd.Aligner(flags=flags) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
+    ref, rcells = oracle_of(w, X=X)
+    assert_same(res, cells, ref, rcells, f"random X={X} flags={flags}")
+
+
+@pytest.mark.parametrize("M,mu,g", [(2, -3, -2), (5, -4, -3), (2, -1, -1), (1, -2, -1)])
+def test_scoring_schemes(xd, M, mu, g):
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=7 * M - mu, n_pairs=120, len_lo=20, len_hi=900, k=17, X=20,
+                                M=M, mu=mu, g=g)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=17, X=20, M=M, mu=mu, g=g)
+    ref, rcells = oracle_of(w, M=M, mu=mu, g=g)
+    assert_same(res, cells, ref, rcells, f"scoring {M},{mu},{g}")
+
+
+def test_unrelated_wide_bands_escalate(xd):
+    """Unrelated continuations widen the band past the lane window (level 1/2 paths)."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=5, n_pairs=60, len_lo=800, len_hi=2500, k=17, X=60, related=0.0)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=17, X=60)
+        st = al.stats()
+    ref, rcells = oracle_of(w, X=60)
+    assert_same(res, cells, ref, rcells, "wide")
+    assert st["escalated"][0] > 0
+
+
+def test_general_path_huge_band(xd):
+    """X large enough that nothing is pruned: band > 1024 -> general kernel."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=9, n_pairs=6, len_lo=1200, len_hi=1500, k=5, X=100000, related=0.0)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=5, X=100000)
+        st = al.stats()
+    ref, rcells = oracle_of(w, X=100000)
+    assert_same(res, cells, ref, rcells, "general")
+    assert st["escalated"][2] > 0
+
+
+def test_ecoli_shaped_sample_full_launch(xd):
+    """Full E. coli-shaped batch in the bench's launch configuration; a sample is checked
+    against the oracle (every 50th pair + the 200 longest), all checked for sanity."""
+    from synth import workload as W
+    w = W.config("ecoli")
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    lens = np.diff(w.offsets)
+    est = np.minimum(w.pairs[:, 2], w.pairs[:, 3]) + np.minimum(lens[w.pairs[:, 0]] - w.pairs[:, 2],
+                                                                 lens[w.pairs[:, 1]] - w.pairs[:, 3])
+    idx = np.unique(np.concatenate([np.arange(0, w.n_pairs, 50), np.argsort(-est)[:200]]))
+    ref, rcells = oracle_of(w, pairs=w.pairs[idx])
+    assert_same(res[idx], cells[idx], ref, rcells, "ecoli sample")
+    # properties at any size: seed inside the reported interval, score <= min span
+    assert np.all(res["a_begin"] <= w.pairs[:, 2]) and np.all(res["a_end"] >= w.pairs[:, 2] + w.k)
+    assert np.all(res["score"] <= np.minimum(res["a_end"] - res["a_begin"], res["b_end"] - res["b_begin"]))
+
+
+@pytest.mark.parametrize("policy,n_ranks,c", [("cells", 1, 1), ("one2all", 3, 2), ("one2one", 5, 2),
+                                              ("opt_one2one", 5, 3)])
+def test_policies_fake_multi_gpu_identical(xd, policy, n_ranks, c):
+    """Logical GPUs = streams on device 0 (no kernel waits on another); results must be
+    identical for every policy and device count, and no device runs two turns at once."""
+    from synth import workload as W
+    w = W.config("cfg1")
+    with xd.Aligner(devices=[0, 0, 0], policy=policy, n_ranks=n_ranks, batch_size=37, subbatches=c) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        tr = al.trace()
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, policy)
+    assert tr["n_pairs"].sum() == w.n_pairs
+    for g in range(3):
+        ev = np.sort(tr[tr["gpu"] == g], order="t0_ms")
+        assert np.all(ev["t0_ms"][1:] >= ev["t1_ms"][:-1]), f"overlapping turns on gpu {g}"
+
+
+def test_device_api_torch_tensors(xd):
+    import torch
+    from synth import workload as W
+    w = W.config("cfg1")
+    dev = torch.device("cuda:0")
+    seq = torch.from_numpy(w.seq).to(dev)
+    off = torch.from_numpy(w.offsets).to(dev)
+    pairs = torch.from_numpy(w.pairs).to(dev)
+    out = torch.zeros((w.n_pairs, 5), dtype=torch.int32, device=dev)
+    cells = torch.zeros(w.n_pairs, dtype=torch.int64, device=dev)
+    with xd.Aligner() as al:
+        al.align_device(seq, off, pairs, out, cells, k=w.k, X=w.X, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    ref, rcells = oracle_of(w)
+    o = out.cpu().numpy()
+    for t, f in enumerate(FIELDS):
+        assert np.array_equal(o[:, t], ref[f]), f
+    assert np.array_equal(cells.cpu().numpy(), rcells)
+
+
+def test_errors(xd):
+    from synth import workload as W
+    w = W.config("tiny")
+    with xd.Aligner() as al:
+        bad = w.seq.copy()
+        bad[5] = ord("N")
+        with pytest.raises(xd.XdropError) as e:
+            al.align(bad, w.offsets, w.pairs, k=w.k, X=w.X)
+        assert e.value.status == -4 and e.value.index == 5
+        p = w.pairs.copy()
+        p[3, 2] = 10 ** 6
+        with pytest.raises(xd.XdropError) as e:
+            al.align(w.seq, w.offsets, p, k=w.k, X=w.X)
+        assert e.value.status == -5 and e.value.index == 3
+        with pytest.raises(xd.XdropError):
+            al.align(w.seq, w.offsets, w.pairs, k=0, X=w.X)
+        with pytest.raises(xd.XdropError):
+            al.align(w.seq, w.offsets, w.pairs, k=17, X=-1)
+        r, c = al.align(w.seq, w.offsets, w.pairs[:0], k=w.k, X=w.X)
+        assert r.shape == (0,)
+        # still usable after errors
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, "after errors")
+
+
+def test_lowercase_and_k31(xd):
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=31, n_pairs=80, len_lo=40, len_hi=600, k=31, X=15)
+    low = w.seq.copy()
+    low[::3] = np.char.lower(low[::3].view("S1")).view(np.uint8)
+    with xd.Aligner() as al:
+        res, cells = al.align(low, w.offsets, w.pairs, k=31, X=15)
+    ref, rcells = oracle_of(w, X=15)
+    assert_same(res, cells, ref, rcells, "lowercase k31")
