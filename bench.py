@@ -1,0 +1,342 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched X-drop hot path (BASELINE.json metric: GCUPS and alignments/s).
+
+One step = one pass of the whole hot path over one batch:
+ASCII->2-bit pack, validation + cost estimate + length-sorted queue, left/right
+band kernels (all escalation levels), combine -- through the C ABI
+(xdrop_align_batch_device) on inputs resident in HBM.  ``e2e`` repeats the
+measurement through xdrop_align_batch with pinned HOST buffers (H2D of the read
+pool + pairs and D2H of the results inside the timed region).
+
+Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun,
+one rank per GPU; pairs are independent, each rank aligns its own shard:
+weak scaling, no data-path collective).  ``--impl reference`` times the CPU
+oracle (the only other place this file executes oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_OPS_PER_CELL = 8          # algorithmic INT32 ops per DP cell
+SM_COUNT_NOMINAL = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="ecoli", help="synth.workload config (BASELINE configs[1] = ecoli)")
+    ap.add_argument("--scale", type=float, default=1.0, help="pair-count scale (tests only)")
+    ap.add_argument("--X", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded oracle sample")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- dist
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def allreduce(x: float, op: str, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------- workload
+def shard_workload(args, rank):
+    """Each rank aligns its own synthetic batch of the named config (seed offset by rank)."""
+    from synth import workload as W
+    base = {"cfg1": 1, "ecoli": 2, "xsweep": 4, "celegans": 5, "tiny": 7}[args.config]
+    return W.config(args.config, scale=args.scale, X=args.X, seed=base + 1000 * rank)
+
+
+def workload_desc(w, args, world):
+    lens = np.diff(w.offsets)
+    return {"workload": f"{w.name} (BASELINE configs[1]: E. coli-shaped, ~10 kb PacBio-like reads, 15% error)"
+            if args.config == "ecoli" else w.name,
+            "pairs_per_gpu": w.n_pairs, "global_pairs": w.n_pairs * world, "reads_per_gpu": int(lens.shape[0]),
+            "mean_read_len": round(float(lens.mean()), 1), "pool_bases_per_gpu": int(w.offsets[-1]),
+            "k": w.k, "X": w.X, "scoring": [w.M, w.mu, w.g],
+            "errors": "1.5% sub / 9% ins / 4.5% del", "parallelism": f"dp{world} (independent shards)",
+            "l2": "flushed between timed steps (256 MiB memset)", "recipe_seed": w.recipe.get("seed")}
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.f:
+            return None
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        finally:
+            try:
+                os.unlink(self.f.name)
+            except Exception:
+                pass
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 8]
+        if not rows:
+            return None
+        sm = np.array([float(r[0]) for r in rows])
+        load = sm[sm > 0.5 * sm.max()] if sm.size else sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": int(sm.size), "power_w_max": max(float(r[2]) for r in rows)}
+
+
+# ---------------------------------------------------------------------- cpu legs
+def oracle_sample(w, seconds: float, rng_seed: int = 0):
+    """Bounded sample of the workload for the oracle: a pilot fixes the rate, then an
+    evenly spaced sample of pairs sized to ~`seconds` of CPU work is timed."""
+    import oracle
+    n = w.n_pairs
+    cores = os.cpu_count() or 1
+    pilot = np.arange(0, n, max(1, n // 64))[:64]
+    t = time.perf_counter()
+    _, c = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[pilot], w.k, w.M, w.mu, w.g, w.X,
+                              nthreads=cores)
+    dt = max(1e-3, time.perf_counter() - t)
+    per_pair = dt / pilot.size
+    m = int(min(n, max(pilot.size, seconds / per_pair)))
+    idx = np.linspace(0, n - 1, m).astype(np.int64)
+    t = time.perf_counter()
+    _, cells = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[idx], w.k, w.M, w.mu, w.g, w.X,
+                                  nthreads=cores)
+    dt = time.perf_counter() - t
+    return {"value": round(float(cells.sum()) / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+            "sample": f"{m} of {n} pairs (evenly spaced), {int(cells.sum())} cells in {dt:.2f} s "
+                      f"on {cores} host threads; alignments/s {m / dt:.1f}",
+            "alignments_per_s": round(m / dt, 2)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    if rank != 0:
+        return
+    w = shard_workload(args, 0)
+    vals = []
+    for step in range(args.warmup + args.steps):
+        r = oracle_sample(w, seconds=max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup))))
+        if step >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    line = {"impl": "reference", "metric": "GCUPS (X-drop DP cells per second)", "value": v, "unit": "GCUPS",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": workload_desc(w, args, world), "ms_per_step": None,
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "alignments_per_s": float(np.median([r["alignments_per_s"] for r in vals]))}
+    emit(line, args)
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(s + "\n")
+
+
+# ----------------------------------------------------------------------- native
+def run_native(args, world, rank, local):
+    import torch
+    import paper_2309_07270_b200 as xd
+
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    w = shard_workload(args, rank)
+    al = xd.Aligner(devices=[local])
+    stream = torch.cuda.current_stream(dev)
+
+    # inputs resident in HBM (value); pinned host copies (e2e)
+    seq_d = torch.from_numpy(w.seq).to(dev)
+    off_d = torch.from_numpy(w.offsets).to(dev)
+    pairs_d = torch.from_numpy(w.pairs).to(dev)
+    out_d = torch.zeros((w.n_pairs, 5), dtype=torch.int32, device=dev)
+    cells_d = torch.zeros(w.n_pairs, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
+
+    def step():
+        al.align_device(seq_d, off_d, pairs_d, out_d, cells_d, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    cells_step = int(cells_d.sum().item())
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    step_ms, l0_ms, stats = [], [], []
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                                   # untimed L2 flush between timed steps
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            st = al.stats()
+            stats.append(st)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    total_ms_max = allreduce(total_ms, "max", world, dev)
+    cells_all = allreduce(float(cells_step * args.steps), "sum", world, dev)
+    pairs_all = allreduce(float(w.n_pairs * args.steps), "sum", world, dev)
+    gcups = cells_all / (total_ms_max * 1e-3) / 1e9
+    aps = pairs_all / (total_ms_max * 1e-3)
+
+    # dominant kernel: band level 0 (lane per extension)
+    lvl_ms = np.mean([s["level_ms"] for s in stats], axis=0)
+    lvl_cells = stats[-1]["level_cells"]
+    dom = int(np.argmax(lvl_ms))
+    dom_names = ["xk::band_merged_kernel<32,8> (levels 0+1: lane/extension + in-kernel warp/extension escalation)", "(merged into level 0)",
+                 "xk::band_kernel<32,32> (warp/extension)", "xk::general_kernel"]
+    achieved_ops = lvl_cells[dom] * ALGO_OPS_PER_CELL / (lvl_ms[dom] * 1e-3)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clocks = clk.summary()
+    sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    # ALU pipe = 16 lanes/clk per SMSP x 4 SMSP x SMs x max clock
+    peak_ops = sms * 4 * 16 * sm_max * 1e6
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_band_kernel.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "achieved": round(achieved_ops / 1e9, 1), "peak": round(peak_ops / 1e9, 1),
+                "unit": "Gop/s", "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
+                "kernel": dom_names[dom], "kernel_ms": round(float(lvl_ms[dom]), 3),
+                "kernel_share_of_step": round(float(lvl_ms[dom]) / (total_ms / args.steps), 4),
+                "ops_per_cell": ALGO_OPS_PER_CELL, "cells_per_launch": int(lvl_cells[dom]),
+                "peak_basis": f"{sms} SMs x 4 SMSP x 16 INT32 lanes/clk (ALU pipe) x {sm_max:.0f} MHz"}
+    try:
+        p_alu, p_dual = al.int32_peak()
+        roofline["measured_int32_issue"] = {"alu_only_gops": round(p_alu / 1e9, 1),
+                                            "alu_plus_fma_gops": round(p_dual / 1e9, 1)}
+    except Exception:
+        pass
+
+    # e2e through the host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        seq_h = torch.from_numpy(w.seq).pin_memory().numpy()
+        off_h = torch.from_numpy(w.offsets).pin_memory().numpy()
+        pairs_h = torch.from_numpy(w.pairs).pin_memory().numpy()
+        al.align(seq_h, off_h, pairs_h, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g)     # warm
+        barrier(world)
+        t0 = time.perf_counter()
+        e_steps = max(1, min(args.steps, 3))
+        for _ in range(e_steps):
+            res_h, cells_h = al.align(seq_h, off_h, pairs_h, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g)
+        e_ms = (time.perf_counter() - t0) * 1e3
+        e_ms_max = allreduce(e_ms, "max", world, dev)
+        e_cells = allreduce(float(int(cells_h.sum()) * e_steps), "sum", world, dev)
+        h2d = int(w.seq.nbytes + w.offsets.nbytes + w.pairs.nbytes)
+        d2h = int(w.n_pairs * (20 + 8))
+        e2e = {"value": round(e_cells / (e_ms_max * 1e-3) / 1e9, 3), "unit": "GCUPS", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e_steps, "ms_per_step": round(e_ms_max / e_steps, 3)}
+        # e2e results must equal the device path's
+        o = out_d.cpu().numpy()
+        assert np.array_equal(o[:, 0], res_h["score"]) and np.array_equal(cells_h, cells_d.cpu().numpy())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = oracle_sample(w, args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": "GCUPS (X-drop DP cells per second; also alignments/s, INT32 roofline fraction)",
+                "value": round(gcups, 3), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": round(total_ms_max / args.steps, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic", "config": workload_desc(w, args, world),
+                "alignments_per_s": round(aps, 1), "cells_per_step": cells_all / args.steps,
+                "e2e": e2e, "gpu_launches": int(sum(s["launches"] for s in stats) * world),
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+                "escalated_per_step": stats[-1]["escalated"][:3],
+                "level_ms": [round(float(x), 3) for x in lvl_ms], "step_ms_all": [round(x, 3) for x in step_ms]}
+        emit(line, args)
+    al.close()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_native(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -59,7 +59,7 @@ struct HostBuf {
 
 // counters block layout (ints)
 enum { C_NITEMS = 0, C_HEAD0 = 1, C_HEAD1 = 2, C_HEAD2 = 3, C_HEAD3 = 4, C_OVF1 = 5, C_OVF2 = 6, C_OVF3 = 7,
-       C_N = 8 };
+       C_DONE0 = 8, C_Q1HEAD = 9, C_N = 10 };
 
 __global__ void init_counters_kernel(int* c, int n_items) {
   if (threadIdx.x < C_N) c[threadIdx.x] = (threadIdx.x == C_NITEMS) ? n_items : 0;
@@ -73,7 +73,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1;
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
       counters, bad, ext, out5, cells, scratch, level_acc;
@@ -103,6 +103,8 @@ int dev_open(DevCtx& D, int dev) {
   D.own_stream = true;
   for (auto& e : D.ev) CK(cudaEventCreate(&e));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l0, xk::band_kernel<1, 32>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 8>, 128, 0));
+  D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_kernel<32, 32>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_gen, xk::general_kernel, 128, 0));
@@ -203,31 +205,34 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     // a5/a6/a7: band levels.  Level 0 = lane per extension (S = 32); level 1 =
     // warp per extension (S = 256); level 2 = warp per extension (S = 1024).
     int* items0 = D.items.as<int>();
-    int* lvl1_items = D.ovf1.as<int>();
-    int* lvl1_count = ctr + C_OVF1;
-    if (fl.force_wide || fl.force_general) {
-      lvl1_items = items0;
-      lvl1_count = ctr + C_NITEMS;
+    int* lvl2_items = D.ovf2.as<int>();
+    int* lvl2_count = ctr + C_OVF2;
+    if (fl.force_general) {
+      // everything goes to the general kernel below
+    } else if (fl.force_wide) {
+      xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEAD1,
+                                                             D.ovf2.as<int>(), ctr + C_OVF2, 1);
+      ++launches;
     } else {
-      xk::band_kernel<1, 32><<<D.sms * D.occ_l0, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEAD0,
-                                                             D.ovf1.as<int>(), ctr + C_OVF1, 0);
+      // levels 0 + 1 in one persistent kernel (in-kernel escalation queue = ovf1)
+      CK(cudaMemsetAsync(D.ovf1.p, 0xff, (size_t)n_items * sizeof(int), s));
+      xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_OVF1, ctr + C_Q1HEAD, ctr + C_OVF2};
+      xk::band_merged_kernel<32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+                                                                    D.ovf1.as<int>(), D.ovf2.as<int>());
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
+    CK(cudaEventRecord(D.ev[9], s));
     int* gen_items = D.ovf3.as<int>();
     int* gen_count = ctr + C_OVF3;
     if (fl.force_general) {
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
     } else {
-      xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, lvl1_items, lvl1_count, ctr + C_HEAD1,
-                                                             D.ovf2.as<int>(), ctr + C_OVF2, 1);
-      CK(cudaEventRecord(D.ev[9], s));
-      xk::band_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, D.ovf2.as<int>(), ctr + C_OVF2,
-                                                              ctr + C_HEAD2, D.ovf3.as<int>(), ctr + C_OVF3, 2);
-      launches += 2;
+      xk::band_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, lvl2_items, lvl2_count, ctr + C_HEAD2,
+                                                              D.ovf3.as<int>(), ctr + C_OVF3, 2);
+      ++launches;
     }
-    if (fl.force_general) CK(cudaEventRecord(D.ev[9], s));
     CK(cudaEventRecord(D.ev[10], s));
     CK(cudaGetLastError());
     // read the validation flags and the general-path count

@@ -120,6 +120,8 @@ template <int G> __device__ __forceinline__ int gmin(int v) {
 }
 
 // ------------------------------------------------------------ band kernel
+constexpr int KEYM = 100;   // argmax key = v * KEYM + (KEYM-1-t): IMAD (FMA pipe), not LEA (ALU)
+
 // State of one extension as seen by one lane of its group.
 template <int C> struct Band {
   int R[2 * C];                 // diagonals K0 + 2C*gl + r, r in [0, 2C)
@@ -135,21 +137,24 @@ template <int C> struct Band {
 };
 
 template <int G, int C>
-__device__ __forceinline__ void band_reload(Band<C>& B, int gl, int arem, int brem, const Problem& P) {
+__device__ __forceinline__ void band_reload(Band<C>& B, int gl, int rem, const Problem& P) {
   const int ia = B.ia0 + C * gl, jb = B.jb0 - C * gl;
   B.Aw = load32c(P.PA, B.sa, B.da, ia);
   B.An = load16(P.PA, B.sa, B.da, ia + 32);
-  B.An2 = load16(P.PA, B.sa, B.da, ia + 32 + arem);
+  B.An2 = load16(P.PA, B.sa, B.da, ia + 32 + rem);
   B.Bw = rev_fields(load32c(P.PB, B.sb, B.db, jb - 31));
   B.Bn = load16(P.PB, B.sb, B.db, jb + 1);
-  B.Bn2 = load16(P.PB, B.sb, B.db, jb + 1 + brem);
+  B.Bn2 = load16(P.PB, B.sb, B.db, jb + 1 + rem);
 }
 
-// One anti-diagonal of parity PAR: the cells of this lane (C of them).
+// One anti-diagonal d of parity PAR: the C cells of this lane, the group
+// reductions (live extent, best and its smallest i), the hull count, and the
+// stream advance to d+1.
 template <int G, int C, int PAR, bool CHECK>
-__device__ __forceinline__ void band_cells_impl(Band<C>& B, int gl, int d, int thr, int qlo, int qhi,
-                                                int& mk, unsigned& dbits, int M, int mu, int g) {
+__device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, int qhi, const Problem& P) {
   constexpr int NR = 2 * C;
+  const int thr = B.best - P.X;
+  const int M = P.M, mu = P.mu, g = P.g;
   const uint64_t x = B.Aw ^ B.Bw;
   int nb = NEGV;
   if constexpr (G > 1) {
@@ -161,8 +166,8 @@ __device__ __forceinline__ void band_cells_impl(Band<C>& B, int gl, int d, int t
       if (gl == G - 1) nb = NEGV;
     }
   }
-  int mkl = NEGV * 64;
-  unsigned bits = 0;
+  int mk = NEGV * KEYM;
+  unsigned dbits = 0;
 #pragma unroll
   for (int tt = 0; tt < C; ++tt) {
     const int r = 2 * tt + PAR;
@@ -179,11 +184,48 @@ __device__ __forceinline__ void band_cells_impl(Band<C>& B, int gl, int d, int t
     }
     v = live ? v : NEGV;
     B.R[r] = v;
-    mkl = max(mkl, v * 64 + (63 - tt));
-    bits = __funnelshift_l((unsigned)v, bits, 1);   // dead cells set the bit (sign)
+    mk = max(mk, v * KEYM + (KEYM - 1 - tt));
+    dbits = __funnelshift_l((unsigned)v, dbits, 1);   // dead cells set the bit (sign)
   }
-  mk = mkl;
-  dbits = bits;
+  // lane live extent (local t); cell tt sits at bit C-1-tt of dbits
+  const unsigned lb = ~dbits & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  int tmin = lb ? (__clz(lb) - (32 - C)) + C * gl : EMIN;
+  int tmax = lb ? (C - __ffs(lb)) + C * gl : EMAX;
+  tmin = gmin<G>(tmin);
+  tmax = gmax<G>(tmax);
+  const int vl = mk / KEYM;
+  int gv, gt;
+  if constexpr (G == 1) {
+    gv = vl; gt = KEYM - 1 - (mk - vl * KEYM);
+  } else {
+    gv = gmax<G>(vl);
+    const unsigned ball = __ballot_sync(FULL, vl == gv);
+    const int grp = (threadIdx.x & 31) / G;
+    const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
+    const int first = __ffs(gb) - 1;
+    gt = __shfl_sync(FULL, C * gl + KEYM - 1 - (mk - vl * KEYM), first, G);
+  }
+  const int ibase = (d + B.K0 + PAR) >> 1;
+  if (B.active) {
+    if (gv > B.best) { B.best = gv; B.istar = ibase + gt; B.jstar = d - B.istar; }
+    // hull of anti-diagonal d (from the live sets of d-1 and d-2)
+    const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
+    const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
+    B.cells += (long long)max(0, hi - lo + 1);
+  }
+  B.minL2 = B.minL1; B.maxL2 = B.maxL1;
+  B.minL1 = (tmin == EMIN) ? EMIN : ibase + tmin;
+  B.maxL1 = (tmax == EMAX) ? EMAX : ibase + tmax;
+  // stream advance for anti-diagonal d+1
+  if constexpr (PAR == 0) {       // even -> odd: a advances (ia0 += 1)
+    B.Aw = (B.Aw >> 2) | ((uint64_t)(B.An & 3u) << 62);
+    B.An >>= 2;
+    B.ia0 += 1;
+  } else {                        // odd -> even: b advances (jb0 += 1)
+    B.Bw = (B.Bw << 2) | (uint64_t)(B.Bn & 3u);
+    B.Bn >>= 2;
+    B.jb0 += 1;
+  }
 }
 
 template <int G, int C>
@@ -212,86 +254,32 @@ __device__ __forceinline__ void band_shift(Band<C>& B, int gl, int dir) {
   }
 }
 
-// Finish one anti-diagonal: reductions, best/argmax, hull count, termination,
-// window management, stream advance.  Returns nothing; updates B.
-template <int G, int C, int PAR>
-__device__ __forceinline__ void band_step(Band<C>& B, int gl, int d, int& arem, int& brem,
-                                          const Problem& P, int level, int* ovf_items, int* ovf_count) {
+// queue push: slot = atomicAdd(tail); store; fence (consumers may be running)
+__device__ __forceinline__ void push_item(int* items, int* tail, int item) {
+  const int pos = atomicAdd(tail, 1);
+  *((volatile int*)items + pos) = item;
+  __threadfence();
+}
+
+// End of a block of two anti-diagonals (d-1 odd, d even): termination,
+// reservoir refill, window management.  The window is checked every two
+// anti-diagonals, so it keeps the live cells of d-1 and d inside [2, 2S-3]
+// (the band grows by at most one diagonal per side per anti-diagonal).
+template <int G, int C>
+__device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& rem, const Problem& P, int level,
+                                               int* push_items, int* push_tail) {
   constexpr int S = G * C;
-  const int thr = B.best - P.X;
-  // boundary: cells with i > m or j > n must be dead (q in [qlo, qhi] valid)
-  const int qlo = d - B.K0 - 2 * B.n;
-  const int qhi = 2 * B.m - d - B.K0;
-  const bool need = B.active && (qlo > 0 || qhi < 2 * S - 1);
-  int mk;
-  unsigned dbits;
-  if (__any_sync(FULL, need))
-    band_cells_impl<G, C, PAR, true>(B, gl, d, thr, qlo, qhi, mk, dbits, P.M, P.mu, P.g);
-  else
-    band_cells_impl<G, C, PAR, false>(B, gl, d, thr, qlo, qhi, mk, dbits, P.M, P.mu, P.g);
-
-  // lane live extent (local t), cell tt sits at bit C-1-tt of dbits
-  const unsigned lb = ~dbits & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
-  int tmin = lb ? (__clz(lb) - (32 - C)) + C * gl : EMIN;
-  int tmax = lb ? (C - __ffs(lb)) + C * gl : EMAX;
-  tmin = gmin<G>(tmin);
-  tmax = gmax<G>(tmax);
-  // best value and the smallest t attaining it
-  int vl = mk >> 6;
-  int gt;
-  int gv;
-  if constexpr (G == 1) {
-    gv = vl; gt = 63 - (mk & 63);
-  } else {
-    gv = gmax<G>(vl);
-    const unsigned ball = __ballot_sync(FULL, vl == gv);
-    const int grp = (threadIdx.x & 31) / G;
-    const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
-    const int first = __ffs(gb) - 1;
-    gt = __shfl_sync(FULL, C * gl + 63 - (mk & 63), first, G);
-  }
-  const int ibase = (d + B.K0 + PAR) >> 1;
-  const int minL0 = (tmin == EMIN) ? EMIN : ibase + tmin;
-  const int maxL0 = (tmax == EMAX) ? EMAX : ibase + tmax;
-  if (B.active) {
-    if (gv > B.best) { B.best = gv; B.istar = ibase + gt; B.jstar = d - B.istar; }
-    // hull of anti-diagonal d (from the live sets of d-1 and d-2)
-    const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
-    const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
-    B.cells += (long long)max(0, hi - lo + 1);
-  }
-  const bool empty0 = (tmin == EMIN), empty1 = (B.minL1 == EMIN);
-  // q-extent of the live cells of d and d-1 in window coordinates
-  int qmn = 1 << 30, qmx = -(1 << 30);
-  if (!empty0) { qmn = 2 * minL0 - d - B.K0; qmx = 2 * maxL0 - d - B.K0; }
-  if (!empty1) { qmn = min(qmn, 2 * B.minL1 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL1 - (d - 1) - B.K0); }
-  B.minL2 = B.minL1; B.maxL2 = B.maxL1;
-  B.minL1 = minL0; B.maxL1 = maxL0;
-
-  // stream advance for anti-diagonal d+1 (uniform over the warp)
-  if constexpr (PAR == 0) {       // a advances: ia0 += 1
-    B.Aw = (B.Aw >> 2) | ((uint64_t)(B.An & 3u) << 62);
-    B.An >>= 2;
-    B.ia0 += 1;
-    if (--arem == 0) {
-      arem = 16;
-      B.An = B.An2;
-      if (B.active) B.An2 = load16(P.PA, B.sa, B.da, B.ia0 + C * gl + 48);
-    }
-  } else {                        // b advances: jb0 += 1
-    B.Bw = (B.Bw << 2) | (uint64_t)(B.Bn & 3u);
-    B.Bn >>= 2;
-    B.jb0 += 1;
-    if (--brem == 0) {
-      brem = 16;
-      B.Bn = B.Bn2;
-      if (B.active) B.Bn2 = load16(P.PB, B.sb, B.db, B.jb0 - C * gl + 17);
+  if (--rem == 0) {
+    rem = 16;
+    B.An = B.An2; B.Bn = B.Bn2;
+    if (B.active) {
+      B.An2 = load16(P.PA, B.sa, B.da, B.ia0 + C * gl + 48);
+      B.Bn2 = load16(P.PB, B.sb, B.db, B.jb0 - C * gl + 17);
     }
   }
-
   if (!B.active) return;
-  const bool done = (empty0 && empty1) || (d >= B.m + B.n);
-  if (done) {
+  const bool e0 = (B.minL1 == EMIN), e1 = (B.minL2 == EMIN);
+  if ((e0 && e1) || d >= B.m + B.n) {
     if (gl == 0) {
       ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
       o.cells = B.cells; o.pad = 0;
@@ -300,31 +288,82 @@ __device__ __forceinline__ void band_step(Band<C>& B, int gl, int d, int& arem, 
     B.active = false;
     return;
   }
-  // window management (uniform within the group)
+  int qmn = 1 << 30, qmx = -(1 << 30);
+  if (!e0) { qmn = 2 * B.minL1 - d - B.K0; qmx = 2 * B.maxL1 - d - B.K0; }
+  if (!e1) { qmn = min(qmn, 2 * B.minL2 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL2 - (d - 1) - B.K0); }
   int dir = 0;
   bool ovf = false;
-  if (qmx >= 2 * S - 2) { if (qmn >= 3) dir = 1; else ovf = true; }
+  if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
   else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
   if (ovf) {
-    if (gl == 0) { const int pos = atomicAdd(ovf_count, 1); ovf_items[pos] = B.item; }
+    if (gl == 0) push_item(push_items, push_tail, B.item);
     B.active = false;
     return;
   }
   if (dir != 0) {
     band_shift<G, C>(B, gl, dir);
     B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
-    band_reload<G, C>(B, gl, arem, brem, P);
+    band_reload<G, C>(B, gl, rem, P);
   }
 }
 
+// Run one extension per group of G lanes (item < 0: idle group).  Warp-collective.
+template <int G, int C>
+__device__ __forceinline__ void band_run(const Problem& P, int item, int level, int* push_items, int* push_tail) {
+  constexpr int S = G * C;
+  const int gl = (threadIdx.x & 31) % G;
+  Band<C> B;
+  B.active = item >= 0;
+  B.item = B.active ? item : 0;
+  if (B.active) {
+    const Geom gm = item_geom(P, B.item);
+    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+  } else {
+    B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
+  }
+  B.K0 = -S;
+  B.ia0 = -S / 2;          // window chars for d = 1 (odd): ia0 = (1+K0+1)/2 - 1
+  B.jb0 = S / 2 - 1;       //                               jb0 = (1-K0-1)/2 - 1
+#pragma unroll
+  for (int r = 0; r < 2 * C; ++r) B.R[r] = NEGV;
+  // origin: d = 0, k = 0 -> q = S -> lane G/2 (r = 0), or lane 0 r = C when G = 1
+  if constexpr (G == 1) B.R[C] = BIAS;
+  else if (gl == G / 2) B.R[0] = BIAS;
+  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1;
+  B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
+  int rem = 16;
+  band_reload<G, C>(B, gl, rem, P);
+  if (B.active && B.m + B.n == 0) {
+    if (gl == 0) {
+      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+      P.ext[B.item] = o;
+    }
+    B.active = false;
+  }
+  int d = 0;
+  while (__any_sync(FULL, B.active)) {
+    // boundary (i > m or j > n) enters the window?  checked for the later step
+    const int d2 = d + 2;
+    const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
+    if (__any_sync(FULL, need)) {
+      band_diag<G, C, 1, true>(B, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P);
+      band_diag<G, C, 0, true>(B, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P);
+    } else {
+      band_diag<G, C, 1, false>(B, gl, d + 1, 0, 0, P);
+      band_diag<G, C, 0, false>(B, gl, d2, 0, 0, P);
+    }
+    d = d2;
+    band_block_end<G, C>(B, gl, d, rem, P, level, push_items, push_tail);
+  }
+}
+
+// Standalone level kernel: persistent warps, 32/G extensions per warp batch.
 template <int G, int C>
 __global__ void __launch_bounds__(128)
 band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
             int* queue_head, int* ovf_items, int* ovf_count, int level) {
-  constexpr int S = G * C;
   constexpr int IPW = 32 / G;
   const int lane = threadIdx.x & 31;
-  const int gl = lane % G;
   const int grp = lane / G;
   const int n_items = *n_items_ptr;
   for (;;) {
@@ -332,43 +371,69 @@ band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_
     if (lane == 0) base = atomicAdd(queue_head, IPW);
     base = __shfl_sync(FULL, base, 0);
     if (base >= n_items) break;
-    Band<C> B;
     const int slot = base + grp;
-    B.active = slot < n_items;
-    B.item = B.active ? items[slot] : 0;
-    if (B.active) {
-      const Geom gm = item_geom(P, B.item);
-      B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
-    } else {
-      B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
-    }
-    B.K0 = -S;
-    B.ia0 = -S / 2;          // window chars for d = 1 (odd): ia0 = (1+K0+1)/2 - 1
-    B.jb0 = S / 2 - 1;       //                               jb0 = (1-K0-1)/2 - 1
-#pragma unroll
-    for (int r = 0; r < 2 * C; ++r) B.R[r] = NEGV;
-    // origin: d = 0, k = 0 -> q = S -> lane G/2 (r = 0), or lane 0 r = C when G = 1
-    if constexpr (G == 1) B.R[C] = BIAS;
-    else if (gl == G / 2) B.R[0] = BIAS;
-    B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1;
-    B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
-    int arem = 16, brem = 16;
-    band_reload<G, C>(B, gl, arem, brem, P);
-    if (B.active && B.m + B.n == 0) {
-      if (gl == 0) {
-        ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
-        P.ext[B.item] = o;
+    band_run<G, C>(P, slot < n_items ? items[slot] : -1, level, ovf_items, ovf_count);
+  }
+}
+
+// Counters of the merged kernel (ints): see xdrop_capi.cu
+struct MergedCtr { int* head0; int* done0; int* q1_tail; int* q1_head; int* ovf2_tail; };
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *((const volatile int*)p); }
+
+// Level 0 (lane per extension, S = 32) and level 1 (warp per extension,
+// S = 32*C1) in ONE persistent kernel: an extension whose band leaves its lane
+// window is pushed to an in-kernel queue and restarted in warp mode by the
+// next warp that looks for work (escalated items take priority), so the wide
+// extensions run while level 0 is still draining instead of as a serial tail.
+template <int C0, int C1>
+__global__ void __launch_bounds__(128)
+band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
+                   int* q1_items, int* ovf2_items) {
+  const int lane = threadIdx.x & 31;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    // 1) escalated items first
+    int it1 = -1;
+    if (lane == 0) {
+      int h = ld_volatile(c.q1_head), t = ld_volatile(c.q1_tail);
+      while (h < t) {
+        const int old = atomicCAS(c.q1_head, h, h + 1);
+        if (old == h) {
+          int v;
+          do { v = ld_volatile(q1_items + h); } while (v < 0);
+          it1 = v;
+          break;
+        }
+        h = old;
+        t = ld_volatile(c.q1_tail);
       }
-      B.active = false;
     }
-    int d = 0;
-    while (__any_sync(FULL, B.active)) {
-      ++d;
-      band_step<G, C, 1>(B, gl, d, arem, brem, P, level, ovf_items, ovf_count);
-      if (!__any_sync(FULL, B.active)) break;
-      ++d;
-      band_step<G, C, 0>(B, gl, d, arem, brem, P, level, ovf_items, ovf_count);
+    it1 = __shfl_sync(FULL, it1, 0);
+    if (it1 >= 0) {
+      band_run<32, C1>(P, it1, 1, ovf2_items, c.ovf2_tail);
+      continue;
     }
+    // 2) a batch of 32 level-0 extensions
+    int base = n_items;
+    if (lane == 0 && ld_volatile(c.head0) < n_items) base = atomicAdd(c.head0, 32);
+    base = __shfl_sync(FULL, base, 0);
+    if (base < n_items) {
+      const int slot = base + lane;
+      band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, q1_items, c.q1_tail);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
+      continue;
+    }
+    // 3) no work visible: finished once every level-0 batch is done and the
+    //    escalation queue is drained (pushes precede their batch's done0 add)
+    int fin = 0;
+    if (lane == 0)
+      fin = ld_volatile(c.done0) >= n_items && ld_volatile(c.q1_head) >= ld_volatile(c.q1_tail);
+    fin = __shfl_sync(FULL, fin, 0);
+    if (fin) break;
+    __nanosleep(1000);
   }
 }
 
