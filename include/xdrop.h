@@ -144,6 +144,7 @@ typedef struct {
   float level_ms[4];      /* CUDA-event time of each band level (0: lane/extension, 1-2: warp/extension, 3: general) */
   int64_t level_cells[4]; /* DP cells of the extensions completed at each level */
   int64_t level_items[4]; /* extensions completed at each level */
+  int64_t long_items;     /* extensions run in the multi-lane "long" mode of level 0 */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 

@@ -109,7 +109,8 @@ class Aligner:
         N.check(N.lib.xdrop_last_stats(self._h, ctypes.byref(s)), "xdrop_last_stats")
         return dict(items=s.items, escalated=list(s.escalated), kernel_ms=s.kernel_ms, total_ms=s.total_ms,
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
-                    level_cells=list(s.level_cells), level_items=list(s.level_items))
+                    level_cells=list(s.level_cells), level_items=list(s.level_items),
+                    long_items=s.long_items)
 
     def sched_stats(self) -> dict:
         s = N.SchedStats()

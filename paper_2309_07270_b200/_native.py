@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libxdrop.so")
+LIB_PATH = os.environ.get("XDROP_LIB") or os.path.join(HERE, "libxdrop.so")   # XDROP_LIB: A/B experiments
 
 # status codes (xdrop_status)
 OK, EINVAL, ENOMEM, ECUDA, EALPHABET, ESEED, ELENGTH, ESTATE, ENODEV = 0, -1, -2, -3, -4, -5, -6, -7, -8
@@ -42,7 +42,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("items", ctypes.c_int64), ("escalated", ctypes.c_int64 * 4), ("cells", ctypes.c_int64),
                 ("kernel_ms", ctypes.c_float), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
                 ("launches", ctypes.c_int64), ("level_ms", ctypes.c_float * 4),
-                ("level_cells", ctypes.c_int64 * 4), ("level_items", ctypes.c_int64 * 4)]
+                ("level_cells", ctypes.c_int64 * 4), ("level_items", ctypes.c_int64 * 4),
+                ("long_items", ctypes.c_int64)]
 
 
 class TraceEvent(ctypes.Structure):

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -59,7 +60,7 @@ struct HostBuf {
 
 // counters block layout (ints)
 enum { C_NITEMS = 0, C_HEAD0 = 1, C_HEAD1 = 2, C_HEAD2 = 3, C_HEAD3 = 4, C_OVF1 = 5, C_OVF2 = 6, C_OVF3 = 7,
-       C_DONE0 = 8, C_Q1HEAD = 9, C_N = 10 };
+       C_DONE0 = 8, C_Q1HEAD = 9, C_HEADL = 10, C_NLONG = 11, C_N = 12 };
 
 __global__ void init_counters_kernel(int* c, int n_items) {
   if (threadIdx.x < C_N) c[threadIdx.x] = (threadIdx.x == C_NITEMS) ? n_items : 0;
@@ -74,6 +75,8 @@ struct DevCtx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1;
+  int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
+  float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
       counters, bad, ext, out5, cells, scratch, level_acc;
@@ -103,7 +106,15 @@ int dev_open(DevCtx& D, int dev) {
   D.own_stream = true;
   for (auto& e : D.ev) CK(cudaEventCreate(&e));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l0, xk::band_kernel<1, 32>, 128, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 8>, 128, 0));
+  if (const char* e = getenv("XDROP_LONG_G")) D.long_g = atoi(e);
+  if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
+  if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
+  if (D.long_g == 2)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16, 8>, 128, 0));
+  else if (D.long_g == 4)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8, 8>, 128, 0));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32, 8>, 128, 0));
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_kernel<32, 32>, 128, 0));
@@ -195,7 +206,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     CK(cudaMemsetAsync(D.hist.p, 0, xk::NBUCKET * sizeof(int), s));
     xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
-    xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>());
+    xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
+                                       (long long)D.sms * D.occ_m * 128, D.long_g ? D.long_alpha : 0.f);
     xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
         D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
     launches += 3;
@@ -216,9 +228,17 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     } else {
       // levels 0 + 1 in one persistent kernel (in-kernel escalation queue = ovf1)
       CK(cudaMemsetAsync(D.ovf1.p, 0xff, (size_t)n_items * sizeof(int), s));
-      xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_OVF1, ctr + C_Q1HEAD, ctr + C_OVF2};
-      xk::band_merged_kernel<32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
-                                                                    D.ovf1.as<int>(), D.ovf2.as<int>());
+      xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_OVF1, ctr + C_Q1HEAD, ctr + C_OVF2,
+                       ctr + C_HEADL, ctr + C_NLONG};
+      if (D.long_g == 2)
+        xk::band_merged_kernel<32, 2, 16, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+                                                                          D.ovf1.as<int>(), D.ovf2.as<int>());
+      else if (D.long_g == 4)
+        xk::band_merged_kernel<32, 4, 8, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+                                                                         D.ovf1.as<int>(), D.ovf2.as<int>());
+      else
+        xk::band_merged_kernel<32, 1, 32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+                                                                          D.ovf1.as<int>(), D.ovf2.as<int>());
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
@@ -247,6 +267,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_OVF1];
     D.st.escalated[1] = hs[C_OVF2];
     D.st.escalated[2] = n_gen;
+    D.st.long_items = hs[C_NLONG];
     if (n_gen > 0) {
       const int64_t stride = XDROP_MAX_READ_LEN + 8;
       const int warps_per_block = 4;

@@ -129,7 +129,8 @@ template <int C> struct Band {
   uint32_t An, An2, Bn, Bn2;    // stream reservoirs (next chars in stream order)
   int64_t sa, sb; int da, db;
   int m, n, K0, ia0, jb0;       // ia0/jb0: char index of global cell t = 0
-  int best, istar, jstar;       // best is biased
+  int best, istar, jstar;       // best is biased (H + BIAS)
+  int dbase;                    // R holds W = H + BIAS + |g| (d - dbase)  (offset space, see band_diag)
   int minL1, maxL1, minL2, maxL2;   // live extents (in i) of d-1 and d-2
   long long cells;
   int item;
@@ -150,11 +151,19 @@ __device__ __forceinline__ void band_reload(Band<C>& B, int gl, int rem, const P
 // One anti-diagonal d of parity PAR: the C cells of this lane, the group
 // reductions (live extent, best and its smallest i), the hull count, and the
 // stream advance to d+1.
+//
+// Offset space: registers hold W_d = H_d + BIAS - g (d - dbase).  Then
+//   H_d(k) = max(H_{d-1}(k-1) + g, H_{d-1}(k+1) + g, H_{d-2}(k) + s)
+// becomes
+//   W_d(k) = max3(W_{d-1}(k-1), W_{d-1}(k+1), W_{d-2}(k) + s - 2g),
+// one VIMNMX3 instead of VIMNMX + VIADDMNMX; the threshold and the best value
+// move by the per-anti-diagonal scalar woff = -g (d - dbase).
 template <int G, int C, int PAR, bool CHECK>
 __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, int qhi, const Problem& P) {
   constexpr int NR = 2 * C;
-  const int thr = B.best - P.X;
-  const int M = P.M, mu = P.mu, g = P.g;
+  const int woff = -P.g * (d - B.dbase);
+  const int thr = B.best - P.X + woff;
+  const int M = P.M - 2 * P.g, mu = P.mu - 2 * P.g;
   const uint64_t x = B.Aw ^ B.Bw;
   int nb = NEGV;
   if constexpr (G > 1) {
@@ -173,10 +182,9 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
     const int r = 2 * tt + PAR;
     const int lft = (r == 0) ? nb : B.R[r == 0 ? 0 : r - 1];
     const int rgt = (r == NR - 1) ? nb : B.R[r == NR - 1 ? 0 : r + 1];
-    const int lu = max(lft, rgt);
     const bool mis = ((x >> (2 * tt)) & 3ull) != 0ull;
     const int dg = B.R[r] + (mis ? mu : M);
-    int v = max(lu + g, dg);
+    int v = __vimax3_s32(lft, rgt, dg);
     bool live = v >= thr;
     if constexpr (CHECK) {
       const int q = 2 * C * gl + r;
@@ -207,7 +215,7 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
   }
   const int ibase = (d + B.K0 + PAR) >> 1;
   if (B.active) {
-    if (gv > B.best) { B.best = gv; B.istar = ibase + gt; B.jstar = d - B.istar; }
+    if (gv - woff > B.best) { B.best = gv - woff; B.istar = ibase + gt; B.jstar = d - B.istar; }
     // hull of anti-diagonal d (from the live sets of d-1 and d-2)
     const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
     const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
@@ -228,14 +236,22 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
   }
 }
 
+// lanes of this lane's group (shifts are taken by one group while the other
+// groups of the warp may not take them)
+template <int G> __device__ __forceinline__ unsigned group_mask() {
+  if constexpr (G == 32) return FULL;
+  else return ((1u << G) - 1u) << (((threadIdx.x & 31) / G) * G);
+}
+
 template <int G, int C>
 __device__ __forceinline__ void band_shift(Band<C>& B, int gl, int dir) {
   constexpr int NR = 2 * C;
+  const unsigned gm = group_mask<G>();
   if (dir > 0) {            // K0 += 2: R[r] <- R[r+2]
     int n0 = NEGV, n1 = NEGV;
     if constexpr (G > 1) {
-      n0 = __shfl_down_sync(FULL, B.R[0], 1, G);
-      n1 = __shfl_down_sync(FULL, B.R[1], 1, G);
+      n0 = __shfl_down_sync(gm, B.R[0], 1, G);
+      n1 = __shfl_down_sync(gm, B.R[1], 1, G);
       if (gl == G - 1) { n0 = NEGV; n1 = NEGV; }
     }
 #pragma unroll
@@ -244,13 +260,39 @@ __device__ __forceinline__ void band_shift(Band<C>& B, int gl, int dir) {
   } else {                  // K0 -= 2: R[r] <- R[r-2]
     int n0 = NEGV, n1 = NEGV;
     if constexpr (G > 1) {
-      n0 = __shfl_up_sync(FULL, B.R[NR - 2], 1, G);
-      n1 = __shfl_up_sync(FULL, B.R[NR - 1], 1, G);
+      n0 = __shfl_up_sync(gm, B.R[NR - 2], 1, G);
+      n1 = __shfl_up_sync(gm, B.R[NR - 1], 1, G);
       if (gl == 0) { n0 = NEGV; n1 = NEGV; }
     }
 #pragma unroll
     for (int r = NR - 1; r >= 2; --r) B.R[r] = B.R[r - 2];
     B.R[0] = n0; B.R[1] = n1;
+  }
+}
+
+// lane mode: shift the register window by 2*K diagonals (R[r] <- R[r + 2K])
+template <int C, int K>
+__device__ __forceinline__ void shift_regs(int (&R)[2 * C]) {
+  if constexpr (K > 0) {
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) R[r] = (r + 2 * K < 2 * C) ? R[(r + 2 * K) % (2 * C)] : NEGV;
+  } else {
+#pragma unroll
+    for (int r = 2 * C - 1; r >= 0; --r) R[r] = (r + 2 * K >= 0) ? R[(r + 2 * K + 2 * C) % (2 * C)] : NEGV;
+  }
+}
+template <int C>
+__device__ __forceinline__ void band_shift_n(Band<C>& B, int s) {
+  switch (s) {
+    case 1: shift_regs<C, 1>(B.R); break;   case -1: shift_regs<C, -1>(B.R); break;
+    case 2: shift_regs<C, 2>(B.R); break;   case -2: shift_regs<C, -2>(B.R); break;
+    case 3: shift_regs<C, 3>(B.R); break;   case -3: shift_regs<C, -3>(B.R); break;
+    case 4: shift_regs<C, 4>(B.R); break;   case -4: shift_regs<C, -4>(B.R); break;
+    case 5: shift_regs<C, 5>(B.R); break;   case -5: shift_regs<C, -5>(B.R); break;
+    case 6: shift_regs<C, 6>(B.R); break;   case -6: shift_regs<C, -6>(B.R); break;
+    case 7: shift_regs<C, 7>(B.R); break;   case -7: shift_regs<C, -7>(B.R); break;
+    case 8: shift_regs<C, 8>(B.R); break;   case -8: shift_regs<C, -8>(B.R); break;
+    default: break;
   }
 }
 
@@ -269,6 +311,12 @@ template <int G, int C>
 __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& rem, const Problem& P, int level,
                                                int* push_items, int* push_tail) {
   constexpr int S = G * C;
+  if (d - B.dbase >= 1024) {      // keep the offset space bounded (|g| * 1024 <= 2^16)
+    const int woff = -P.g * (d - B.dbase);
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) B.R[r] -= woff;
+    B.dbase = d;
+  }
   if (--rem == 0) {
     rem = 16;
     B.An = B.An2; B.Bn = B.Bn2;
@@ -291,19 +339,40 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
   int qmn = 1 << 30, qmx = -(1 << 30);
   if (!e0) { qmn = 2 * B.minL1 - d - B.K0; qmx = 2 * B.maxL1 - d - B.K0; }
   if (!e1) { qmn = min(qmn, 2 * B.minL2 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL2 - (d - 1) - B.K0); }
-  int dir = 0;
-  bool ovf = false;
-  if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
-  else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
-  if (ovf) {
-    if (gl == 0) push_item(push_items, push_tail, B.item);
-    B.active = false;
-    return;
-  }
-  if (dir != 0) {
-    band_shift<G, C>(B, gl, dir);
-    B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
-    band_reload<G, C>(B, gl, rem, P);
+  if constexpr (G == 1) {
+    // lane mode: when the live band nears an edge, re-centre it in one move
+    // (shift by 2s diagonals, |s| <= 8) so shifts stay rare.
+    if (qmx >= 2 * S - 2 || qmn <= 1) {
+      const int s_lo = (qmx - 2 * S + 4) >> 1;            // ceil((qmx - 2S + 3) / 2)
+      const int s_hi = (qmn - 2) >> 1;                     // floor((qmn - 2) / 2)
+      if (s_lo > s_hi) {
+        push_item(push_items, push_tail, B.item);
+        B.active = false;
+        return;
+      }
+      int sh = (((qmn + qmx) >> 1) - S) >> 1;              // centre of the band -> centre of the window
+      sh = min(max(sh, s_lo), s_hi);
+      sh = min(max(sh, -8), 8);
+      if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
+      band_shift_n<C>(B, sh);
+      B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
+      band_reload<G, C>(B, gl, rem, P);
+    }
+  } else {
+    int dir = 0;
+    bool ovf = false;
+    if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
+    else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
+    if (ovf) {
+      if (gl == 0) push_item(push_items, push_tail, B.item);
+      B.active = false;
+      return;
+    }
+    if (dir != 0) {
+      band_shift<G, C>(B, gl, dir);
+      B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
+      band_reload<G, C>(B, gl, rem, P);
+    }
   }
 }
 
@@ -329,7 +398,7 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
   // origin: d = 0, k = 0 -> q = S -> lane G/2 (r = 0), or lane 0 r = C when G = 1
   if constexpr (G == 1) B.R[C] = BIAS;
   else if (gl == G / 2) B.R[0] = BIAS;
-  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1;
+  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
   int rem = 16;
   band_reload<G, C>(B, gl, rem, P);
@@ -377,21 +446,31 @@ band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_
 }
 
 // Counters of the merged kernel (ints): see xdrop_capi.cu
-struct MergedCtr { int* head0; int* done0; int* q1_tail; int* q1_head; int* ovf2_tail; };
+struct MergedCtr { int* head0; int* done0; int* q1_tail; int* q1_head; int* ovf2_tail; int* head_long; int* n_long; };
 
 __device__ __forceinline__ int ld_volatile(const int* p) { return *((const volatile int*)p); }
 
-// Level 0 (lane per extension, S = 32) and level 1 (warp per extension,
-// S = 32*C1) in ONE persistent kernel: an extension whose band leaves its lane
-// window is pushed to an in-kernel queue and restarted in warp mode by the
-// next warp that looks for work (escalated items take priority), so the wide
-// extensions run while level 0 is still draining instead of as a serial tail.
-template <int C0, int C1>
-__global__ void __launch_bounds__(128)
+// Levels 0 and 1 in ONE persistent kernel.
+//  * long extensions (the first n_long of the length-sorted queue; n_long is
+//    set on the device from the batch's total work per resident lane, see
+//    scan_kernel) run GL lanes per extension (CL cells each, same 32-cell
+//    window) so their anti-diagonal chain -- the critical path of the whole
+//    launch -- is GL times shorter per step;
+//  * the rest run one lane per extension (C0 cells);
+//  * an extension whose band leaves its window is pushed to an in-kernel queue
+//    and restarted in warp mode (32 x C1 cells) by the next warp that looks for
+//    work (escalated items first), so wide extensions run while level 0 is
+//    still draining instead of as a serial tail.
+#ifndef XDROP_MERGED_MINBLOCKS
+#define XDROP_MERGED_MINBLOCKS 3
+#endif
+template <int C0, int GL, int CL, int C1>
+__global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
 band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                    int* q1_items, int* ovf2_items) {
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
+  const int n_long = min(*c.n_long, n_items);
   for (;;) {
     // 1) escalated items first
     int it1 = -1;
@@ -414,9 +493,24 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       band_run<32, C1>(P, it1, 1, ovf2_items, c.ovf2_tail);
       continue;
     }
-    // 2) a batch of 32 level-0 extensions
+    // 2) long extensions, 32/GL per warp
+    if constexpr (GL > 1) {
+      int base = n_long;
+      if (lane == 0 && ld_volatile(c.head_long) < n_long) base = atomicAdd(c.head_long, 32 / GL);
+      base = __shfl_sync(FULL, base, 0);
+      if (base < n_long) {
+        const int slot = base + lane / GL;
+        band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, q1_items, c.q1_tail);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.done0, min(32 / GL, n_long - base));
+        continue;
+      }
+    }
+    // 3) the rest, 32 per warp (lane per extension)
+    const int first = (GL > 1) ? n_long : 0;
     int base = n_items;
-    if (lane == 0 && ld_volatile(c.head0) < n_items) base = atomicAdd(c.head0, 32);
+    if (lane == 0 && first + ld_volatile(c.head0) < n_items) base = first + atomicAdd(c.head0, 32);
     base = __shfl_sync(FULL, base, 0);
     if (base < n_items) {
       const int slot = base + lane;
@@ -426,7 +520,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
       continue;
     }
-    // 3) no work visible: finished once every level-0 batch is done and the
+    // 4) no work visible: finished once every level-0 batch is done and the
     //    escalation queue is drained (pushes precede their batch's done0 add)
     int fin = 0;
     if (lane == 0)
@@ -559,19 +653,30 @@ __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict_
   atomicAdd(&hist[min(wr >> BUCKET_SHIFT, NBUCKET - 1)], 1);
 }
 
-// exclusive scan of the histogram in DESCENDING bucket order (one block of 1024)
-__global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ cursor) {
+// exclusive scan of the histogram in DESCENDING bucket order (one block of
+// 1024), plus the long-extension cut: extensions whose cost w exceeds
+// alpha * (total w / resident lanes) -- i.e. whose own anti-diagonal chain is
+// a sizeable fraction of the whole launch's per-lane work -- form the prefix
+// [0, n_long) of the sorted queue (alpha <= 0 disables the long mode).
+__global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ cursor, int* __restrict__ n_long,
+                            long long lanes, float alpha) {
   __shared__ int part[1024];
+  __shared__ unsigned long long wsum[32];
   constexpr int PER = NBUCKET / 1024;
   const int t = threadIdx.x;
   int local[PER];
   int s = 0;
+  unsigned long long ws = 0;
 #pragma unroll
   for (int u = 0; u < PER; ++u) {       // thread t owns descending ranks t*PER .. t*PER+PER-1
     const int b = NBUCKET - 1 - (t * PER + u);
-    local[u] = s; s += hist[b];
+    const int h = hist[b];
+    local[u] = s; s += h;
+    ws += (unsigned long long)h * (unsigned long long)((b << BUCKET_SHIFT) + (1 << (BUCKET_SHIFT - 1)));
   }
   part[t] = s;
+  for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(FULL, ws, o);
+  if ((t & 31) == 0) wsum[t >> 5] = ws;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
     const int v = t >= o ? part[t - o] : 0;
@@ -582,6 +687,18 @@ __global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ curs
   const int base = part[t] - s;
 #pragma unroll
   for (int u = 0; u < PER; ++u) cursor[NBUCKET - 1 - (t * PER + u)] = base + local[u];
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < 32; ++w) tot += wsum[w];
+    int nl = 0;
+    if (alpha > 0.f && lanes > 0) {
+      const double thr_w = (double)alpha * (double)tot / (double)lanes;
+      const long long tb = (long long)(thr_w / (double)(1 << BUCKET_SHIFT)) + 1;   // buckets fully above
+      if (tb < NBUCKET) nl = cursor[tb] + hist[tb];   // items in buckets >= tb
+    }
+    *n_long = nl;
+  }
 }
 
 __global__ void scatter_kernel(const int* __restrict__ wcost, int64_t n_items, int* __restrict__ cursor,

@@ -182,3 +182,20 @@ def test_lowercase_and_k31(xd):
         res, cells = al.align(low, w.offsets, w.pairs, k=31, X=15)
     ref, rcells = oracle_of(w, X=15)
     assert_same(res, cells, ref, rcells, "lowercase k31")
+
+
+@pytest.mark.parametrize("long_g", ["0", "2", "4"])
+@pytest.mark.parametrize("X", [0, 7, 15, 40])
+def test_long_mode_multilane(xd, long_g, X, monkeypatch):
+    """Every extension through the multi-lane long mode (alpha tiny) or none (G=0)."""
+    from synth import workload as W
+    monkeypatch.setenv("XDROP_LONG_G", long_g)
+    monkeypatch.setenv("XDROP_LONG_ALPHA", "0.0001")
+    w = W.random_pairs_workload(seed=300 + X, n_pairs=120, len_lo=0, len_hi=1500, k=13, X=X)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
+        st = al.stats()
+    ref, rcells = oracle_of(w, X=X)
+    assert_same(res, cells, ref, rcells, f"long G={long_g} X={X}")
+    if long_g != "0":
+        assert st["long_items"] > 0
