@@ -110,11 +110,11 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
   if (D.long_g == 2)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 2, 16, 8>, 128, 0));
   else if (D.long_g == 4)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 4, 8, 8>, 128, 0));
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 1, 32, 8>, 128, 0));
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_kernel<32, 32>, 128, 0));
@@ -198,6 +198,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   P.PB = PB; P.offB = offB; P.nB = nB;
   P.pairs = pairs; P.n_pairs = n_pairs;
   P.M = p.match; P.mu = p.mismatch; P.g = p.gap; P.X = p.xdrop; P.k = p.k;
+  P.keym = 1 << xk::KEYSH;
   P.ext = D.ext.as<ExtOut>();
 
   int* ctr = D.counters.as<int>();
@@ -231,13 +232,13 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_OVF1, ctr + C_Q1HEAD, ctr + C_OVF2,
                        ctr + C_HEADL, ctr + C_NLONG};
       if (D.long_g == 2)
-        xk::band_merged_kernel<32, 2, 16, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+        xk::band_merged_kernel<XDROP_C0, 2, 16, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
                                                                           D.ovf1.as<int>(), D.ovf2.as<int>());
       else if (D.long_g == 4)
-        xk::band_merged_kernel<32, 4, 8, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+        xk::band_merged_kernel<XDROP_C0, 4, 8, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
                                                                          D.ovf1.as<int>(), D.ovf2.as<int>());
       else
-        xk::band_merged_kernel<32, 1, 32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
+        xk::band_merged_kernel<XDROP_C0, 1, 32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
                                                                           D.ovf1.as<int>(), D.ovf2.as<int>());
       ++launches;
     }

@@ -30,7 +30,7 @@
 namespace xk {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int NEGV = -(1 << 24);   // value of a dead cell (biased domain)
+constexpr int NEGV = -(1 << 23);   // value of a dead cell (biased domain); NEGV * 128 fits int32
 constexpr int BIAS = 1 << 21;      // stored value = H + BIAS; live values are > 0
 constexpr int GUARD = 2048;        // bases of padding before/after the packed pool
 constexpr int EMIN = 1 << 29;      // extent of an empty live set: [EMIN, EMAX]
@@ -51,6 +51,7 @@ struct Problem {
   const uint32_t* PB; const int64_t* offB; int64_t nB;
   const PairDesc* pairs; int64_t n_pairs;
   int M, mu, g, X, k;
+  int keym;          // 128: argmax key multiplier, passed at run time so ptxas keeps it an IMAD (FMA pipe)
   ExtOut* ext;
 };
 
@@ -120,7 +121,26 @@ template <int G> __device__ __forceinline__ int gmin(int v) {
 }
 
 // ------------------------------------------------------------ band kernel
-constexpr int KEYM = 100;   // argmax key = v * KEYM + (KEYM-1-t): IMAD (FMA pipe), not LEA (ALU)
+// argmax key = v * 128 + (127 - t): formed with IMAD (FMA pipe; P.keym), decoded with one shift
+constexpr int KEYSH = 7;
+
+// max over k[0..N) as a tree of 3-input VIMNMX3 (depth log3 N, not N/2)
+template <int N>
+__device__ __forceinline__ int tree_max3(int (&k)[N]) {
+  if constexpr (N == 1) {
+    return k[0];
+  } else {
+    constexpr int M = (N + 2) / 3;
+    int t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (3 * i + 2 < N) t[i] = __vimax3_s32(k[3 * i], k[3 * i + 1], k[3 * i + 2]);
+      else if (3 * i + 1 < N) t[i] = max(k[3 * i], k[3 * i + 1]);
+      else t[i] = k[3 * i];
+    }
+    return tree_max3<M>(t);
+  }
+}
 
 // State of one extension as seen by one lane of its group.
 template <int C> struct Band {
@@ -131,6 +151,7 @@ template <int C> struct Band {
   int m, n, K0, ia0, jb0;       // ia0/jb0: char index of global cell t = 0
   int best, istar, jstar;       // best is biased (H + BIAS)
   int dbase;                    // R holds W = H + BIAS + |g| (d - dbase)  (offset space, see band_diag)
+  int thrW;                     // pruning threshold of the next anti-diagonal, in W space
   int minL1, maxL1, minL2, maxL2;   // live extents (in i) of d-1 and d-2
   long long cells;
   int item;
@@ -156,14 +177,19 @@ __device__ __forceinline__ void band_reload(Band<C>& B, int gl, int rem, const P
 //   H_d(k) = max(H_{d-1}(k-1) + g, H_{d-1}(k+1) + g, H_{d-2}(k) + s)
 // becomes
 //   W_d(k) = max3(W_{d-1}(k-1), W_{d-1}(k+1), W_{d-2}(k) + s - 2g),
-// one VIMNMX3 instead of VIMNMX + VIADDMNMX; the threshold and the best value
-// move by the per-anti-diagonal scalar woff = -g (d - dbase).
+// one VIMNMX3 instead of VIMNMX + VIADDMNMX.  The threshold is carried in W
+// space: thrW_{d+1} = max(thrW_d, vmaxW_d - X) - g, the only bookkeeping on
+// the anti-diagonal-to-anti-diagonal critical path; the live mask and the
+// argmax key are reduced as trees so a lone warp's step is issue-bound.
 template <int G, int C, int PAR, bool CHECK>
 __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, int qhi, const Problem& P) {
   constexpr int NR = 2 * C;
-  const int woff = -P.g * (d - B.dbase);
-  const int thr = B.best - P.X + woff;
+  constexpr int NCH = (C % 4 == 0 && C >= 8) ? 4 : 1;   // live-mask chains
+  constexpr int CL = C / NCH;                            // cells per chain
+  static_assert(C % NCH == 0, "chain split");
+  const int thr = B.thrW;
   const int M = P.M - 2 * P.g, mu = P.mu - 2 * P.g;
+  const int keym = P.keym;
   const uint64_t x = B.Aw ^ B.Bw;
   int nb = NEGV;
   if constexpr (G > 1) {
@@ -175,8 +201,11 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
       if (gl == G - 1) nb = NEGV;
     }
   }
-  int mk = NEGV * KEYM;
-  unsigned dbits = 0;
+  const int two = keym >> (KEYSH - 1);  // 2, opaque: keeps ch * two + s an IMAD
+  int key[C];
+  int ch[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) ch[c] = 0;
 #pragma unroll
   for (int tt = 0; tt < C; ++tt) {
     const int r = 2 * tt + PAR;
@@ -185,42 +214,54 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
     const bool mis = ((x >> (2 * tt)) & 3ull) != 0ull;
     const int dg = B.R[r] + (mis ? mu : M);
     int v = __vimax3_s32(lft, rgt, dg);
-    bool live = v >= thr;
+    // prune on the FMA pipe: s = -1 if v < thr (dead) else 0; a dead value is
+    // forced negative (v | 0xFF800000), below every threshold (> 2^20) for good
+    int sd = __mulhi(v - thr, 2);
     if constexpr (CHECK) {
       const int q = 2 * C * gl + r;
-      live = live && (q >= qlo) && (q <= qhi);
+      sd = (q >= qlo && q <= qhi) ? sd : -1;
     }
-    v = live ? v : NEGV;
+    v = v | (sd & (int)0xFF800000);
     B.R[r] = v;
-    mk = max(mk, v * KEYM + (KEYM - 1 - tt));
-    dbits = __funnelshift_l((unsigned)v, dbits, 1);   // dead cells set the bit (sign)
+    key[tt] = v * keym + (127 - tt);
+    ch[tt / CL] = ch[tt / CL] * two + sd;  // accumulates -(dead bits)
   }
-  // lane live extent (local t); cell tt sits at bit C-1-tt of dbits
-  const unsigned lb = ~dbits & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
-  int tmin = lb ? (__clz(lb) - (32 - C)) + C * gl : EMIN;
-  int tmax = lb ? (C - __ffs(lb)) + C * gl : EMAX;
-  tmin = gmin<G>(tmin);
-  tmax = gmax<G>(tmax);
-  const int vl = mk / KEYM;
+  unsigned dbits = 0;                   // cell tt at bit C-1-tt
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) dbits = (dbits << CL) + (unsigned)(-ch[c]);
+  const int mk = tree_max3<C>(key);
+  // ---- critical path: next threshold
+  const int vl = mk >> KEYSH;           // best W value of this lane (NEGV if none live)
   int gv, gt;
   if constexpr (G == 1) {
-    gv = vl; gt = KEYM - 1 - (mk - vl * KEYM);
+    gv = vl; gt = 127 - (mk & 127);
   } else {
     gv = gmax<G>(vl);
     const unsigned ball = __ballot_sync(FULL, vl == gv);
     const int grp = (threadIdx.x & 31) / G;
     const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
     const int first = __ffs(gb) - 1;
-    gt = __shfl_sync(FULL, C * gl + KEYM - 1 - (mk - vl * KEYM), first, G);
+    gt = __shfl_sync(FULL, C * gl + 127 - (mk & 127), first, G);
   }
+  B.thrW = max(thr, gv - P.X) - P.g;
+  // ---- off the critical path: live extent, best / argmax, hull count
+  const unsigned lb = ~dbits & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  int tmin = (__clz(lb) - (32 - C)) + C * gl;
+  int tmax = (C - __ffs(lb)) + C * gl;
+  tmin = lb ? tmin : EMIN;
+  tmax = lb ? tmax : EMAX;
+  tmin = gmin<G>(tmin);
+  tmax = gmax<G>(tmax);
   const int ibase = (d + B.K0 + PAR) >> 1;
-  if (B.active) {
-    if (gv - woff > B.best) { B.best = gv - woff; B.istar = ibase + gt; B.jstar = d - B.istar; }
-    // hull of anti-diagonal d (from the live sets of d-1 and d-2)
-    const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
-    const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
-    B.cells += (long long)max(0, hi - lo + 1);
-  }
+  const int woff = -P.g * (d - B.dbase);
+  const bool up = B.active && (gv - woff > B.best);
+  B.best = up ? gv - woff : B.best;
+  B.istar = up ? ibase + gt : B.istar;
+  B.jstar = up ? d - ibase - gt : B.jstar;
+  // hull of anti-diagonal d (from the live sets of d-1 and d-2)
+  const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
+  const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
+  B.cells += (B.active && hi >= lo) ? (long long)(hi - lo + 1) : 0ll;
   B.minL2 = B.minL1; B.maxL2 = B.maxL1;
   B.minL1 = (tmin == EMIN) ? EMIN : ibase + tmin;
   B.maxL1 = (tmax == EMAX) ? EMAX : ibase + tmax;
@@ -315,6 +356,7 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
     const int woff = -P.g * (d - B.dbase);
 #pragma unroll
     for (int r = 0; r < 2 * C; ++r) B.R[r] -= woff;
+    B.thrW -= woff;
     B.dbase = d;
   }
   if (--rem == 0) {
@@ -399,6 +441,7 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
   if constexpr (G == 1) B.R[C] = BIAS;
   else if (gl == G / 2) B.R[0] = BIAS;
   B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
+  B.thrW = BIAS - P.X - P.g;     // threshold of anti-diagonal 1 in W space (woff_1 = -g)
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
   int rem = 16;
   band_reload<G, C>(B, gl, rem, P);
@@ -461,6 +504,9 @@ __device__ __forceinline__ int ld_volatile(const int* p) { return *((const volat
 //    and restarted in warp mode (32 x C1 cells) by the next warp that looks for
 //    work (escalated items first), so wide extensions run while level 0 is
 //    still draining instead of as a serial tail.
+#ifndef XDROP_C0
+#define XDROP_C0 32
+#endif
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
