@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -80,8 +81,8 @@ struct DevCtx {
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
       counters, bad, ext, out5, cells, scratch, level_acc;
-  // host staging
-  HostBuf h_small;
+  // host staging (pinned)
+  HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
   xdrop_stats st{};
   int64_t err_index = -1;
@@ -132,7 +133,7 @@ void dev_close(DevCtx& D) {
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
                  &D.cells, &D.scratch, &D.level_acc};
   for (Buf* b : bufs) b->release();
-  D.h_small.release();
+  D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
   if (D.own_stream && D.stream) cudaStreamDestroy(D.stream);
   D.stream = nullptr;
@@ -471,17 +472,23 @@ struct DevSession {
     uploaded = true;
     return 0;
   }
-  // align pairs[idx[0..n)] -> out[idx[t]]
+  // align pairs[idx[0..n)] -> out[idx[t]]; idx == nullptr means pairs[0..n) (no gather/scatter:
+  // descriptors and results move straight between the caller's buffers and the device)
   int run(const int64_t* idx, int64_t n) {
     DevCtx& d = *D;
     CKR(upload());
-    std::vector<xdrop_pair> sub((size_t)n);
-    for (int64_t t = 0; t < n; ++t) sub[(size_t)t] = hb->pairs[idx[t]];
     CKR(d.pairs.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(xdrop_pair)));
     CKR(d.out5.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(xdrop_result)));
     CKR(d.cells.ensure((size_t)std::max<int64_t>(n, 1) * 8));
-    if (n > 0)
-      CK(cudaMemcpyAsync(d.pairs.p, sub.data(), (size_t)n * sizeof(xdrop_pair), cudaMemcpyHostToDevice, d.stream));
+    if (idx) {
+      CKR(d.h_pairs.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(xdrop_pair)));
+      xdrop_pair* sub = reinterpret_cast<xdrop_pair*>(d.h_pairs.p);
+      for (int64_t t = 0; t < n; ++t) sub[t] = hb->pairs[idx[t]];
+      if (n > 0)
+        CK(cudaMemcpyAsync(d.pairs.p, sub, (size_t)n * sizeof(xdrop_pair), cudaMemcpyHostToDevice, d.stream));
+    } else if (n > 0) {
+      CK(cudaMemcpyAsync(d.pairs.p, hb->pairs, (size_t)n * sizeof(xdrop_pair), cudaMemcpyHostToDevice, d.stream));
+    }
     const xdrop_seqs* A = hb->A;
     const xdrop_seqs* B = hb->B;
     const char* sA = d.asciiA.as<char>();
@@ -493,19 +500,26 @@ struct DevSession {
                           d.stream, hb->fl, !packed);
     if (rc == 0 || rc != XDROP_EALPHABET) packed = true;
     if (rc) {
-      if (d.err_index >= 0 && rc != XDROP_EALPHABET) d.err_index = idx[d.err_index];
+      if (d.err_index >= 0 && rc != XDROP_EALPHABET && idx) d.err_index = idx[d.err_index];
       return rc;
     }
-    std::vector<xdrop_result> res((size_t)n);
-    std::vector<int64_t> cl((size_t)n);
-    if (n > 0) {
-      CK(cudaMemcpyAsync(res.data(), d.out5.p, (size_t)n * sizeof(xdrop_result), cudaMemcpyDeviceToHost, d.stream));
-      CK(cudaMemcpyAsync(cl.data(), d.cells.p, (size_t)n * 8, cudaMemcpyDeviceToHost, d.stream));
+    if (n == 0) return 0;
+    if (!idx) {
+      CK(cudaMemcpyAsync(hb->out, d.out5.p, (size_t)n * sizeof(xdrop_result), cudaMemcpyDeviceToHost, d.stream));
+      if (hb->cells_out)
+        CK(cudaMemcpyAsync(hb->cells_out, d.cells.p, (size_t)n * 8, cudaMemcpyDeviceToHost, d.stream));
       CK(cudaStreamSynchronize(d.stream));
+      return 0;
     }
+    CKR(d.h_res.ensure((size_t)n * (sizeof(xdrop_result) + 8)));
+    xdrop_result* res = reinterpret_cast<xdrop_result*>(d.h_res.p);
+    int64_t* cl = reinterpret_cast<int64_t*>(res + n);
+    CK(cudaMemcpyAsync(res, d.out5.p, (size_t)n * sizeof(xdrop_result), cudaMemcpyDeviceToHost, d.stream));
+    CK(cudaMemcpyAsync(cl, d.cells.p, (size_t)n * 8, cudaMemcpyDeviceToHost, d.stream));
+    CK(cudaStreamSynchronize(d.stream));
     for (int64_t t = 0; t < n; ++t) {
-      hb->out[idx[t]] = res[(size_t)t];
-      if (hb->cells_out) hb->cells_out[idx[t]] = cl[(size_t)t];
+      hb->out[idx[t]] = res[t];
+      if (hb->cells_out) hb->cells_out[idx[t]] = cl[t];
     }
     return 0;
   }
@@ -556,6 +570,18 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   std::vector<DevSession> sess((size_t)m);
   for (int g = 0; g < m; ++g) { sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; }
 
+  if (m == 1 && ctx->opts.policy == XDROP_POLICY_CELLS) {   // one device: no partition, no gather
+    const auto t0 = std::chrono::steady_clock::now();
+    rc = sess[0].run(nullptr, n_pairs);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ctx->sched = xdrop_sched_stats{};
+    ctx->sched.turns = 1; ctx->sched.span_ms = ms; ctx->sched.busy_ms[0] = ms; ctx->sched.max_concurrent = 1;
+    ctx->sched.n_events = 1;
+    ctx->trace.assign(1, xdrop_trace_event{0, 0, 0, 0, n_pairs, 0.0, ms});
+    if (rc) { ctx->err_index = sess[0].D->err_index; return rc; }
+    ctx->st = ctx->devs[0].st;
+    return 0;
+  }
   // estimated cost per pair (a3): anti-diagonals ~ min prefix + min suffix
   std::vector<int64_t> w((size_t)n_pairs);
   for (int64_t t = 0; t < n_pairs; ++t) {
