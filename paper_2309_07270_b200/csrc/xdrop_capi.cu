@@ -60,11 +60,17 @@ struct HostBuf {
 };
 
 // counters block layout (ints)
-enum { C_NITEMS = 0, C_HEAD0 = 1, C_HEAD1 = 2, C_HEAD2 = 3, C_HEAD3 = 4, C_OVF1 = 5, C_OVF2 = 6, C_OVF3 = 7,
-       C_DONE0 = 8, C_Q1HEAD = 9, C_HEADL = 10, C_NLONG = 11, C_N = 12 };
+enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
+       C_P1, C_Q1T, C_Q1H, C_DONE1,                         // T1 record pool / queue
+       C_P2, C_Q2T, C_Q2H,                                  // T2
+       C_P3, C_Q3T, C_HEAD3,                                // S = 1024 launch
+       C_P4, C_Q4T, C_HEAD4,                                // CTA launch (S = 4096)
+       C_GEN, C_HEADG, C_HEADW, C_N };
+// host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
+enum { HS_BAD = 32, HS_LVL = 48, HS_BYTES = 512 };
 
 __global__ void init_counters_kernel(int* c, int n_items) {
-  if (threadIdx.x < C_N) c[threadIdx.x] = (threadIdx.x == C_NITEMS) ? n_items : 0;
+  for (int i = threadIdx.x; i < C_N; i += blockDim.x) c[i] = (i == C_NITEMS) ? n_items : 0;
 }
 __global__ void init_bad_kernel(unsigned long long* bad) {
   if (threadIdx.x < 2) bad[threadIdx.x] = ~0ull;
@@ -75,12 +81,12 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_cta = 1;
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl;
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -111,18 +117,20 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
   if (D.long_g == 2)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 2, 16, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
   else if (D.long_g == 4)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 4, 8, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8>, 128, 0));
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<XDROP_C0, 1, 32, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32>, 128, 0));
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_kernel<32, 32>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_resume_kernel<32, 32>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_gen, xk::general_kernel, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta, xk::band_cta_kernel<256, 16>, 256, 0));
+  D.occ_cta = std::max(1, D.occ_cta);
   D.occ_l0 = std::max(1, D.occ_l0); D.occ_l1 = std::max(1, D.occ_l1);
   D.occ_l2 = std::max(1, D.occ_l2); D.occ_gen = std::max(1, D.occ_gen);
-  CKR(D.h_small.ensure(256));
+  CKR(D.h_small.ensure(HS_BYTES));
   return 0;
 }
 
@@ -131,7 +139,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -216,59 +224,71 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   }
   CK(cudaEventRecord(D.ev[2], s));
   if (n_pairs > 0) {
-    // a5/a6/a7: band levels.  Level 0 = lane per extension (S = 32); level 1 =
-    // warp per extension (S = 256); level 2 = warp per extension (S = 1024).
+    // a5/a6/a7: band tiers (xdrop_kernels.cuh): T0 lane (S = 32) / long multi-lane (S = 32),
+    // T1 lane pair (S = 64), T2 warp (S = 256) in one persistent kernel; checkpoints of T2
+    // resume in a warp with S = 1024; beyond that the unbounded kernel restarts the extension.
     int* items0 = D.items.as<int>();
-    int* lvl2_items = D.ovf2.as<int>();
-    int* lvl2_count = ctr + C_OVF2;
+    const int64_t cap1 = std::min<int64_t>(n_items, 1 << 20), cap2 = std::min<int64_t>(n_items, 1 << 18),
+                  cap3 = std::min<int64_t>(n_items, 1 << 17);
+    const int64_t cap4 = std::min<int64_t>(n_items, 1 << 14);
+    const int rec1 = xk::HDR + 2 * 32, rec2 = xk::HDR + 2 * 64, rec3 = xk::HDR + 2 * 256, rec4 = xk::HDR + 2 * 1024;
+    CKR(D.pool1.ensure((size_t)std::max<int64_t>(cap1, 1) * rec1 * sizeof(int)));
+    CKR(D.pool2.ensure((size_t)std::max<int64_t>(cap2, 1) * rec2 * sizeof(int)));
+    CKR(D.pool3.ensure((size_t)std::max<int64_t>(cap3, 1) * rec3 * sizeof(int)));
+    CKR(D.pool4.ensure((size_t)std::max<int64_t>(cap4, 1) * rec4 * sizeof(int)));
+    CKR(D.q4.ensure((size_t)std::max<int64_t>(cap4, 1) * sizeof(int)));
+    CKR(D.genl.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+    CK(cudaMemsetAsync(D.ovf1.p, 0xff, (size_t)n_items * sizeof(int), s));
+    CK(cudaMemsetAsync(D.ovf2.p, 0xff, (size_t)n_items * sizeof(int), s));
+    int* gen = D.genl.as<int>();
+    xk::Esc e1{D.pool1.as<int>(), rec1, (int)cap1, ctr + C_P1, D.ovf1.as<int>(), ctr + C_Q1T, gen, ctr + C_GEN};
+    xk::Esc e2{D.pool2.as<int>(), rec2, (int)cap2, ctr + C_P2, D.ovf2.as<int>(), ctr + C_Q2T, gen, ctr + C_GEN};
+    xk::Esc e3{D.pool3.as<int>(), rec3, (int)cap3, ctr + C_P3, D.ovf3.as<int>(), ctr + C_Q3T, gen, ctr + C_GEN};
+    xk::Esc e4{D.pool4.as<int>(), rec4, (int)cap4, ctr + C_P4, D.q4.as<int>(), ctr + C_Q4T, gen, ctr + C_GEN};
+    xk::Esc eg{nullptr, 0, 0, ctr + C_HEADW, nullptr, nullptr, gen, ctr + C_GEN};   // always falls back
     if (fl.force_general) {
-      // everything goes to the general kernel below
+      // everything goes to the unbounded kernel below
     } else if (fl.force_wide) {
-      xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEAD1,
-                                                             D.ovf2.as<int>(), ctr + C_OVF2, 1);
+      xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW, e3, 1);
       ++launches;
     } else {
-      // levels 0 + 1 in one persistent kernel (in-kernel escalation queue = ovf1)
-      CK(cudaMemsetAsync(D.ovf1.p, 0xff, (size_t)n_items * sizeof(int), s));
-      xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_OVF1, ctr + C_Q1HEAD, ctr + C_OVF2,
-                       ctr + C_HEADL, ctr + C_NLONG};
+      xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
+                       ctr + C_Q2H};
       if (D.long_g == 2)
-        xk::band_merged_kernel<XDROP_C0, 2, 16, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
-                                                                          D.ovf1.as<int>(), D.ovf2.as<int>());
+        xk::band_merged_kernel<32, 2, 16><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
       else if (D.long_g == 4)
-        xk::band_merged_kernel<XDROP_C0, 4, 8, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
-                                                                         D.ovf1.as<int>(), D.ovf2.as<int>());
+        xk::band_merged_kernel<32, 4, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
       else
-        xk::band_merged_kernel<XDROP_C0, 1, 32, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc,
-                                                                          D.ovf1.as<int>(), D.ovf2.as<int>());
+        xk::band_merged_kernel<32, 1, 32><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
     CK(cudaEventRecord(D.ev[9], s));
-    int* gen_items = D.ovf3.as<int>();
-    int* gen_count = ctr + C_OVF3;
+    int* gen_items = gen;
+    int* gen_count = ctr + C_GEN;
     if (fl.force_general) {
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
     } else {
-      xk::band_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, lvl2_items, lvl2_count, ctr + C_HEAD2,
-                                                              D.ovf3.as<int>(), ctr + C_OVF3, 2);
-      ++launches;
+      xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
+      xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e4, ctr + C_HEAD4, eg, 2);
+      launches += 2;
     }
     CK(cudaEventRecord(D.ev[10], s));
     CK(cudaGetLastError());
-    // read the validation flags and the general-path count
+    // read the validation flags and the unbounded-path count
     int* hs = reinterpret_cast<int*>(D.h_small.p);
     CK(cudaMemcpyAsync(hs, ctr, C_N * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hs + 16, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + HS_BAD, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + 16);
+    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + HS_BAD);
     if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
     if (bad[1] != ~0ull) { D.err_index = (int64_t)bad[1]; return XDROP_ESEED; }
-    const int n_gen = fl.force_general ? (int)n_items : hs[C_OVF3];
-    D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_OVF1];
-    D.st.escalated[1] = hs[C_OVF2];
-    D.st.escalated[2] = n_gen;
+    const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
+    D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_P1];
+    D.st.escalated[1] = hs[C_P2];
+    D.st.escalated[2] = hs[C_P3];
+    D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
     if (n_gen > 0) {
       const int64_t stride = XDROP_MAX_READ_LEN + 8;
@@ -277,14 +297,14 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       nwarps = ((nwarps + warps_per_block - 1) / warps_per_block) * warps_per_block;
       CKR(D.scratch.ensure((size_t)nwarps * 3 * stride * sizeof(int)));
       xk::general_kernel<<<(unsigned)(nwarps / warps_per_block), 128, 0, s>>>(
-          P, gen_items, gen_count, ctr + C_HEAD3, D.scratch.as<int>(), stride, 3);
+          P, gen_items, gen_count, ctr + C_HEADG, D.scratch.as<int>(), stride, 3);
       ++launches;
     }
   } else {
     int* hs = reinterpret_cast<int*>(D.h_small.p);
-    CK(cudaMemcpyAsync(hs + 16, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hs + HS_BAD, D.bad.p, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + 16);
+    const unsigned long long* bad = reinterpret_cast<const unsigned long long*>(hs + HS_BAD);
     if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
   }
   CK(cudaEventRecord(D.ev[3], s));
@@ -292,7 +312,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::combine_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         P, out5, cells, D.level_acc.as<unsigned long long>());
     ++launches;
-    CK(cudaMemcpyAsync(reinterpret_cast<int*>(D.h_small.p) + 32, D.level_acc.p, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(reinterpret_cast<int*>(D.h_small.p) + HS_LVL, D.level_acc.p, 64, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaEventRecord(D.ev[4], s));
   CK(cudaGetLastError());
@@ -306,7 +326,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     cudaEventElapsedTime(&ms, D.ev[8], D.ev[9]); D.st.level_ms[1] = ms;
     cudaEventElapsedTime(&ms, D.ev[9], D.ev[10]); D.st.level_ms[2] = ms;
     cudaEventElapsedTime(&ms, D.ev[10], D.ev[3]); D.st.level_ms[3] = ms;
-    const unsigned long long* acc = reinterpret_cast<const unsigned long long*>(reinterpret_cast<int*>(D.h_small.p) + 32);
+    const unsigned long long* acc = reinterpret_cast<const unsigned long long*>(reinterpret_cast<int*>(D.h_small.p) + HS_LVL);
     for (int l = 0; l < 4; ++l) { D.st.level_cells[l] = (int64_t)acc[l]; D.st.level_items[l] = (int64_t)acc[4 + l]; }
     D.st.cells = D.st.level_cells[0] + D.st.level_cells[1] + D.st.level_cells[2] + D.st.level_cells[3];
   }

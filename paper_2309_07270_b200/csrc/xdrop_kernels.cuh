@@ -337,11 +337,56 @@ __device__ __forceinline__ void band_shift_n(Band<C>& B, int s) {
   }
 }
 
+// ---------------------------------------------------------------- escalation
+// An extension whose live band outgrows its window is CHECKPOINTED, not
+// restarted: the group writes a record (scalars + the two live anti-diagonals
+// of its window) to a pool and publishes the record slot on a queue; the next
+// tier resumes it at the same anti-diagonal in a wider window.  The record
+// holds everything the recurrence reads, so resumption is exact.
+__device__ __forceinline__ int ld_volatile(const int* p) { return *((const volatile int*)p); }
+
+struct Esc {
+  int* pool;        // records of rec_ints ints (HDR header ints + 2*S_src cells)
+  int rec_ints;
+  int cap;          // records available in the pool (0: always fall back)
+  int* pool_tail;   // records allocated
+  int* q;           // published record slots (pre-set to -1)
+  int* q_tail;
+  int* fb_items;    // pool full: the item restarts in the unbounded kernel
+  int* fb_tail;
+};
+constexpr int HDR = 32;
+
 // queue push: slot = atomicAdd(tail); store; fence (consumers may be running)
 __device__ __forceinline__ void push_item(int* items, int* tail, int item) {
   const int pos = atomicAdd(tail, 1);
   *((volatile int*)items + pos) = item;
   __threadfence();
+}
+
+template <int G, int C>
+__device__ __forceinline__ void band_save(const Band<C>& B, int gl, int d, const Esc& e) {
+  constexpr int S = G * C;
+  const unsigned gm = group_mask<G>();
+  int slot = 0;
+  if (gl == 0) slot = atomicAdd(e.pool_tail, 1);
+  if constexpr (G > 1) slot = __shfl_sync(gm, slot, 0, G);
+  if (slot >= e.cap) {
+    if (gl == 0) push_item(e.fb_items, e.fb_tail, B.item);
+    return;
+  }
+  int* rec = e.pool + (size_t)slot * e.rec_ints;
+  if (gl == 0) {
+    rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrW; rec[5] = B.best;
+    rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
+    rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = S;
+    rec[15] = (int)(B.cells & 0xffffffffll); rec[16] = (int)(B.cells >> 32);
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * C; ++r) rec[HDR + 2 * C * gl + r] = B.R[r];
+  __threadfence();
+  if constexpr (G > 1) __syncwarp(gm);
+  if (gl == 0) push_item(e.q, e.q_tail, slot);
 }
 
 // End of a block of two anti-diagonals (d-1 odd, d even): termination,
@@ -350,7 +395,7 @@ __device__ __forceinline__ void push_item(int* items, int* tail, int item) {
 // (the band grows by at most one diagonal per side per anti-diagonal).
 template <int G, int C>
 __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& rem, const Problem& P, int level,
-                                               int* push_items, int* push_tail) {
+                                               const Esc& esc) {
   constexpr int S = G * C;
   if (d - B.dbase >= 1024) {      // keep the offset space bounded (|g| * 1024 <= 2^16)
     const int woff = -P.g * (d - B.dbase);
@@ -388,7 +433,7 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
       const int s_lo = (qmx - 2 * S + 4) >> 1;            // ceil((qmx - 2S + 3) / 2)
       const int s_hi = (qmn - 2) >> 1;                     // floor((qmn - 2) / 2)
       if (s_lo > s_hi) {
-        push_item(push_items, push_tail, B.item);
+        band_save<G, C>(B, gl, d, esc);
         B.active = false;
         return;
       }
@@ -406,7 +451,7 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
     if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
     else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
     if (ovf) {
-      if (gl == 0) push_item(push_items, push_tail, B.item);
+      band_save<G, C>(B, gl, d, esc);
       B.active = false;
       return;
     }
@@ -418,19 +463,46 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
   }
 }
 
-// Run one extension per group of G lanes (item < 0: idle group).  Warp-collective.
+// anti-diagonal loop from each group's own B.d (resumed groups of a warp may sit
+// at different anti-diagonals; all are even at block boundaries)
 template <int G, int C>
-__device__ __forceinline__ void band_run(const Problem& P, int item, int level, int* push_items, int* push_tail) {
+__device__ __forceinline__ void band_loop(Band<C>& B, int gl, int& d, int& rem, const Problem& P, int level,
+                                          const Esc& esc) {
+  constexpr int S = G * C;
+  while (__any_sync(FULL, B.active)) {
+    // boundary (i > m or j > n) enters the window?  checked for the later step
+    const int d2 = d + 2;
+    const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
+    if (__any_sync(FULL, need)) {
+      band_diag<G, C, 1, true>(B, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P);
+      band_diag<G, C, 0, true>(B, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P);
+    } else {
+      band_diag<G, C, 1, false>(B, gl, d + 1, 0, 0, P);
+      band_diag<G, C, 0, false>(B, gl, d2, 0, 0, P);
+    }
+    d = d2;
+    band_block_end<G, C>(B, gl, d, rem, P, level, esc);
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void band_idle(Band<C>& B) {
+  B.active = false; B.item = 0;
+  B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
+}
+
+// Run one extension from its seed per group of G lanes (item < 0: idle group).  Warp-collective.
+template <int G, int C>
+__device__ __forceinline__ void band_run(const Problem& P, int item, int level, const Esc& esc) {
   constexpr int S = G * C;
   const int gl = (threadIdx.x & 31) % G;
   Band<C> B;
-  B.active = item >= 0;
-  B.item = B.active ? item : 0;
-  if (B.active) {
+  if (item >= 0) {
+    B.active = true; B.item = item;
     const Geom gm = item_geom(P, B.item);
     B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
   } else {
-    B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
+    band_idle(B);
   }
   B.K0 = -S;
   B.ia0 = -S / 2;          // window chars for d = 1 (odd): ia0 = (1+K0+1)/2 - 1
@@ -453,27 +525,50 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
     B.active = false;
   }
   int d = 0;
-  while (__any_sync(FULL, B.active)) {
-    // boundary (i > m or j > n) enters the window?  checked for the later step
-    const int d2 = d + 2;
-    const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
-    if (__any_sync(FULL, need)) {
-      band_diag<G, C, 1, true>(B, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P);
-      band_diag<G, C, 0, true>(B, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P);
-    } else {
-      band_diag<G, C, 1, false>(B, gl, d + 1, 0, 0, P);
-      band_diag<G, C, 0, false>(B, gl, d2, 0, 0, P);
-    }
-    d = d2;
-    band_block_end<G, C>(B, gl, d, rem, P, level, push_items, push_tail);
-  }
+  band_loop<G, C>(B, gl, d, rem, P, level, esc);
 }
 
-// Standalone level kernel: persistent warps, 32/G extensions per warp batch.
+// Resume one checkpointed extension per group (rec == nullptr: idle group) in a
+// window of S = G*C >= the record's; the old window lands in the middle.
+template <int G, int C>
+__device__ __forceinline__ void band_resume(const Problem& P, const int* rec, int level, const Esc& esc) {
+  constexpr int S = G * C;
+  const int gl = (threadIdx.x & 31) % G;
+  Band<C> B;
+  int d = 0;
+  if (rec) {
+    B.active = true; B.item = rec[0];
+    const Geom gm = item_geom(P, B.item);
+    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+    d = rec[1];
+    const int s_src = rec[14];
+    const int sh = S - s_src;                      // K0' = K0 - sh (sh >= 0, even)
+    B.K0 = rec[2] - sh; B.dbase = rec[3]; B.thrW = rec[4]; B.best = rec[5];
+    B.istar = rec[6]; B.jstar = rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
+    B.maxL2 = rec[11]; B.ia0 = rec[12] - sh / 2; B.jb0 = rec[13] + sh / 2;
+    B.cells = (long long)(unsigned)rec[15] | ((long long)rec[16] << 32);
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) {
+      const int q = 2 * C * gl + r - sh;
+      B.R[r] = (q >= 0 && q < 2 * s_src) ? rec[HDR + q] : NEGV;
+    }
+  } else {
+    band_idle(B);
+    B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1; B.dbase = 0; B.thrW = 0; B.best = 0;
+    B.istar = 0; B.jstar = 0; B.cells = 0; B.minL1 = EMIN; B.maxL1 = EMAX; B.minL2 = EMIN; B.maxL2 = EMAX;
+#pragma unroll
+    for (int r = 0; r < 2 * C; ++r) B.R[r] = NEGV;
+  }
+  int rem = 16;
+  band_reload<G, C>(B, gl, rem, P);
+  band_loop<G, C>(B, gl, d, rem, P, level, esc);
+}
+
+// Standalone kernel, fresh extensions: persistent warps, 32/G per warp batch.
 template <int G, int C>
 __global__ void __launch_bounds__(128)
-band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
-            int* queue_head, int* ovf_items, int* ovf_count, int level) {
+band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, int* queue_head,
+            Esc esc, int level) {
   constexpr int IPW = 32 / G;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G;
@@ -484,96 +579,345 @@ band_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_
     base = __shfl_sync(FULL, base, 0);
     if (base >= n_items) break;
     const int slot = base + grp;
-    band_run<G, C>(P, slot < n_items ? items[slot] : -1, level, ovf_items, ovf_count);
+    band_run<G, C>(P, slot < n_items ? items[slot] : -1, level, esc);
+  }
+}
+
+// Standalone kernel resuming checkpointed extensions (records of `src`).
+template <int G, int C>
+__global__ void __launch_bounds__(128)
+band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
+  constexpr int IPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int n = *src.q_tail;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(queue_head, IPW);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= n) break;
+    const int slot = base + grp;
+    const int* rec = slot < n ? src.pool + (size_t)src.q[slot] * src.rec_ints : nullptr;
+    band_resume<G, C>(P, rec, level, esc);
   }
 }
 
 // Counters of the merged kernel (ints): see xdrop_capi.cu
-struct MergedCtr { int* head0; int* done0; int* q1_tail; int* q1_head; int* ovf2_tail; int* head_long; int* n_long; };
+struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head; };
 
-__device__ __forceinline__ int ld_volatile(const int* p) { return *((const volatile int*)p); }
+// claim up to `want` published entries of a queue (lane 0 only); returns the
+// first claimed index and sets k (0: nothing claimed)
+__device__ __forceinline__ int claim(int* head, const int* tail, int want, bool partial, int& k) {
+  k = 0;
+  int h = ld_volatile(head);
+  for (;;) {
+    const int t = ld_volatile(tail);
+    const int avail = t - h;
+    if (avail <= 0 || (avail < want && !partial)) return 0;
+    const int kk = min(want, avail);
+    const int old = atomicCAS(head, h, h + kk);
+    if (old == h) { k = kk; return h; }
+    h = old;
+  }
+}
+__device__ __forceinline__ int wait_entry(const int* q, int i) {
+  int v;
+  do { v = ld_volatile(q + i); } while (v < 0);
+  return v;
+}
 
-// Levels 0 and 1 in ONE persistent kernel.
-//  * long extensions (the first n_long of the length-sorted queue; n_long is
-//    set on the device from the batch's total work per resident lane, see
-//    scan_kernel) run GL lanes per extension (CL cells each, same 32-cell
-//    window) so their anti-diagonal chain -- the critical path of the whole
-//    launch -- is GL times shorter per step;
-//  * the rest run one lane per extension (C0 cells);
-//  * an extension whose band leaves its window is pushed to an in-kernel queue
-//    and restarted in warp mode (32 x C1 cells) by the next warp that looks for
-//    work (escalated items first), so wide extensions run while level 0 is
-//    still draining instead of as a serial tail.
-#ifndef XDROP_C0
-#define XDROP_C0 32
-#endif
+// Tiers 0-2 in ONE persistent kernel.
+//  T0  fresh extensions: the longest (the first n_long of the length-sorted
+//      queue; n_long is set on the device from the batch's total work per
+//      resident lane, see scan_kernel) run GL lanes per extension (CL cells,
+//      same 32-cell window) so their anti-diagonal chain -- the launch's
+//      critical path -- is GL times shorter per step; the rest run one lane
+//      per extension (C0 = 32 cells).
+//  T1  checkpointed T0 extensions resume two lanes per extension (S = 64),
+//      16 per warp, as soon as 16 are queued (or T0 has no work left).
+//  T2  checkpointed T1 extensions resume one warp per extension (S = 256).
+//  T2 overflows are checkpointed for the separate S = 1024 launch.
+// Escalated work takes priority, so it runs while T0 drains, not as a tail.
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
-template <int C0, int GL, int CL, int C1>
+template <int C0, int GL, int CL>
 __global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
 band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
-                   int* q1_items, int* ovf2_items) {
+                   Esc e1, Esc e2, Esc e3) {
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
+  const int first = (GL > 1) ? n_long : 0;
   for (;;) {
-    // 1) escalated items first
-    int it1 = -1;
-    if (lane == 0) {
-      int h = ld_volatile(c.q1_head), t = ld_volatile(c.q1_tail);
-      while (h < t) {
-        const int old = atomicCAS(c.q1_head, h, h + 1);
-        if (old == h) {
-          int v;
-          do { v = ld_volatile(q1_items + h); } while (v < 0);
-          it1 = v;
-          break;
-        }
-        h = old;
-        t = ld_volatile(c.q1_tail);
+    // T2: one checkpointed extension per warp
+    {
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.q2_head, e2.q_tail, 1, true, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        int slot = 0;
+        if (lane == 0) slot = wait_entry(e2.q, h);
+        slot = __shfl_sync(FULL, slot, 0);
+        band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        continue;
       }
     }
-    it1 = __shfl_sync(FULL, it1, 0);
-    if (it1 >= 0) {
-      band_run<32, C1>(P, it1, 1, ovf2_items, c.ovf2_tail);
-      continue;
+    // T1: 16 checkpointed extensions per warp (partial batches once T0 is drained)
+    {
+      const bool t0_drained = ld_volatile(c.head_long) >= n_long && first + ld_volatile(c.head0) >= n_items;
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 16, t0_drained, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        const int g = lane >> 1;
+        int slot = -1;
+        if (g < k && (lane & 1) == 0) slot = wait_entry(e1.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~1);
+        band_resume<2, 32>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.done1, k);
+        continue;
+      }
     }
-    // 2) long extensions, 32/GL per warp
+    // T0: long extensions, 32/GL per warp
     if constexpr (GL > 1) {
       int base = n_long;
       if (lane == 0 && ld_volatile(c.head_long) < n_long) base = atomicAdd(c.head_long, 32 / GL);
       base = __shfl_sync(FULL, base, 0);
       if (base < n_long) {
         const int slot = base + lane / GL;
-        band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, q1_items, c.q1_tail);
+        band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(c.done0, min(32 / GL, n_long - base));
         continue;
       }
     }
-    // 3) the rest, 32 per warp (lane per extension)
-    const int first = (GL > 1) ? n_long : 0;
+    // T0: the rest, 32 per warp (lane per extension)
     int base = n_items;
     if (lane == 0 && first + ld_volatile(c.head0) < n_items) base = first + atomicAdd(c.head0, 32);
     base = __shfl_sync(FULL, base, 0);
     if (base < n_items) {
       const int slot = base + lane;
-      band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, q1_items, c.q1_tail);
+      band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1);
       __threadfence();
       __syncwarp();
       if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
       continue;
     }
-    // 4) no work visible: finished once every level-0 batch is done and the
-    //    escalation queue is drained (pushes precede their batch's done0 add)
+    // no work visible: finished once T0 is done (=> T1's queue is final), T1 is
+    // done (=> T2's queue is final) and T2's queue is drained
     int fin = 0;
-    if (lane == 0)
-      fin = ld_volatile(c.done0) >= n_items && ld_volatile(c.q1_head) >= ld_volatile(c.q1_tail);
+    if (lane == 0) {
+      if (ld_volatile(c.done0) >= n_items) {
+        const int t1 = ld_volatile(e1.q_tail);
+        if (ld_volatile(c.done1) >= t1 && ld_volatile(c.q1_head) >= t1)
+          fin = ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
+      }
+    }
     fin = __shfl_sync(FULL, fin, 0);
     if (fin) break;
     __nanosleep(1000);
+  }
+}
+
+// ------------------------------------------------------------ CTA path
+// One extension per thread block ("CTA per pair" for the widest bands): NT
+// threads x CC cells = S cells (2S diagonals) in registers, the same cell update
+// as band_diag; neighbours across warp boundaries and the per-anti-diagonal
+// reductions go through shared memory, one barrier per anti-diagonal (buffers
+// double-buffered by anti-diagonal parity).  Resumes checkpoints of the S = 1024
+// warp level; an extension wider than S restarts in the unbounded kernel.
+template <int NT, int CC>
+__global__ void __launch_bounds__(NT)
+band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
+  constexpr int S = NT * CC, NR = 2 * CC, NW = NT / 32;
+  constexpr int NCH = 4, CL = CC / NCH;
+  static_assert(CC % 4 == 0 && CC <= 32, "CC");
+  __shared__ int edgeL[2][NW], edgeR[2][NW];   // lane 0's R[0], lane 31's R[NR-1] per warp
+  __shared__ int red[2][NW][4];                // tmin, tmax, vmax, t* per warp
+  __shared__ int sh_next[NW][2];               // window shift hand-over across warps
+  __shared__ int s_q;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int n = *src.q_tail;
+  const int keym = P.keym, two = keym >> (KEYSH - 1);
+  for (;;) {
+    if (t == 0) s_q = atomicAdd(queue_head, 1);
+    __syncthreads();
+    const int qi = s_q;
+    __syncthreads();
+    if (qi >= n) return;
+    const int* rec = src.pool + (size_t)src.q[qi] * src.rec_ints;
+    // ---- resume (as band_resume with G = NT)
+    const int item = rec[0];
+    const Geom gm = item_geom(P, item);
+    int d = rec[1];
+    const int s_src = rec[14], shv = S - s_src;
+    int K0 = rec[2] - shv, dbase = rec[3], thrW = rec[4], best = rec[5], istar = rec[6], jstar = rec[7];
+    int minL1 = rec[8], maxL1 = rec[9], minL2 = rec[10], maxL2 = rec[11];
+    int ia0 = rec[12] - shv / 2, jb0 = rec[13] + shv / 2;
+    long long cells = (long long)(unsigned)rec[15] | ((long long)rec[16] << 32);
+    int R[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int q = NR * t + r - shv;
+      R[r] = (q >= 0 && q < 2 * s_src) ? rec[HDR + q] : NEGV;
+    }
+    uint64_t Aw, Bw;
+    uint32_t An, An2, Bn, Bn2;
+    int rem = 16;
+    auto reload = [&]() {
+      const int ia = ia0 + CC * t, jb = jb0 - CC * t;
+      Aw = load32c(P.PA, gm.sa, gm.da, ia);
+      An = load16(P.PA, gm.sa, gm.da, ia + 32);
+      An2 = load16(P.PA, gm.sa, gm.da, ia + 32 + rem);
+      Bw = rev_fields(load32c(P.PB, gm.sb, gm.db, jb - 31));
+      Bn = load16(P.PB, gm.sb, gm.db, jb + 1);
+      Bn2 = load16(P.PB, gm.sb, gm.db, jb + 1 + rem);
+    };
+    reload();
+    if (lane == 0) edgeL[d & 1][w] = R[0];        // read by anti-diagonal d+1
+    if (lane == 31) edgeR[d & 1][w] = R[NR - 1];
+    __syncthreads();
+    bool active = true;
+    while (active) {
+#pragma unroll
+      for (int par = 1; par >= 0; --par) {         // odd anti-diagonal, then even
+        ++d;
+        const int pb = (d - 1) & 1, cb = d & 1;      // previous / current buffers
+        const int M2 = P.M - 2 * P.g, mu2 = P.mu - 2 * P.g;
+        const int qlo = d - K0 - 2 * gm.n, qhi = 2 * gm.m - d - K0;
+        const uint64_t x = Aw ^ Bw;
+        int nb;
+        if (par == 0) { nb = __shfl_up_sync(FULL, R[NR - 1], 1); if (lane == 0) nb = w > 0 ? edgeR[pb][w - 1] : NEGV; }
+        else { nb = __shfl_down_sync(FULL, R[0], 1); if (lane == 31) nb = w < NW - 1 ? edgeL[pb][w + 1] : NEGV; }
+        int key[CC];
+        int ch[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) ch[c] = 0;
+#pragma unroll
+        for (int tt = 0; tt < CC; ++tt) {
+          const int r = 2 * tt + par;
+          const int lft = (r == 0) ? nb : R[r == 0 ? 0 : r - 1];
+          const int rgt = (r == NR - 1) ? nb : R[r >= NR - 1 ? 0 : r + 1];
+          const bool mis = ((x >> (2 * tt)) & 3ull) != 0ull;
+          int v = __vimax3_s32(lft, rgt, R[r] + (mis ? mu2 : M2));
+          const int q = NR * t + r;
+          int sd = __mulhi(v - thrW, 2);
+          sd = (q >= qlo && q <= qhi) ? sd : -1;
+          v = v | (sd & (int)0xFF800000);
+          R[r] = v;
+          key[tt] = v * keym + (127 - tt);
+          ch[tt / CL] = ch[tt / CL] * two + sd;
+        }
+        unsigned dbits = 0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) dbits = (dbits << CL) + (unsigned)(-ch[c]);
+        const int mk = tree_max3<CC>(key);
+        const int vl = mk >> KEYSH;
+        const unsigned lb = ~dbits & (CC == 32 ? 0xffffffffu : ((1u << CC) - 1u));
+        const int tmin = lb ? (__clz(lb) - (32 - CC)) + CC * t : EMIN;
+        const int tmax = lb ? (CC - __ffs(lb)) + CC * t : EMAX;
+        // warp reductions, then across warps through shared memory
+        const int wv = __reduce_max_sync(FULL, vl);
+        const unsigned ball = __ballot_sync(FULL, vl == wv);
+        const int wgt = __shfl_sync(FULL, CC * t + 127 - (mk & 127), __ffs(ball) - 1);
+        const int wmin = __reduce_min_sync(FULL, tmin), wmax = __reduce_max_sync(FULL, tmax);
+        if (lane == 0) { red[cb][w][0] = wmin; red[cb][w][1] = wmax; red[cb][w][2] = wv; red[cb][w][3] = wgt;
+                         edgeL[cb][w] = R[0]; }
+        if (lane == 31) edgeR[cb][w] = R[NR - 1];
+        // stream advance for d+1
+        if (par == 0) { Aw = (Aw >> 2) | ((uint64_t)(An & 3u) << 62); An >>= 2; ia0 += 1; }
+        else { Bw = (Bw << 2) | (uint64_t)(Bn & 3u); Bn >>= 2; jb0 += 1; }
+        __syncthreads();
+        int gv = NEGV, gt = 0, gmn = EMIN, gmx = EMAX;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+          const int v = red[cb][k][2];
+          if (v > gv) { gv = v; gt = red[cb][k][3]; }
+          gmn = min(gmn, red[cb][k][0]); gmx = max(gmx, red[cb][k][1]);
+        }
+        thrW = max(thrW, gv - P.X) - P.g;
+        const int ibase = (d + K0 + par) >> 1;
+        const int woff = -P.g * (d - dbase);
+        if (gv - woff > best) { best = gv - woff; istar = ibase + gt; jstar = d - istar; }
+        const int lo = max(max(0, d - gm.n), min(minL1, minL2 + 1));
+        const int hi = min(min(gm.m, d), max(maxL1, maxL2) + 1);
+        cells += hi >= lo ? (long long)(hi - lo + 1) : 0ll;
+        minL2 = minL1; maxL2 = maxL1;
+        minL1 = gmn == EMIN ? EMIN : ibase + gmn;
+        maxL1 = gmx == EMAX ? EMAX : ibase + gmx;
+      }
+      // ---- block end (uniform over the block)
+      if (d - dbase >= 1024) {
+        const int woff = -P.g * (d - dbase);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) R[r] -= woff;
+        thrW -= woff; dbase = d;
+        // the edge copies for anti-diagonal d+1 are in shared memory: rebase them too
+        __syncthreads();
+        if (lane == 0) edgeL[d & 1][w] = R[0];
+        if (lane == 31) edgeR[d & 1][w] = R[NR - 1];
+        __syncthreads();
+      }
+      if (--rem == 0) {
+        rem = 16; An = An2; Bn = Bn2;
+        An2 = load16(P.PA, gm.sa, gm.da, ia0 + CC * t + 48);
+        Bn2 = load16(P.PB, gm.sb, gm.db, jb0 - CC * t + 17);
+      }
+      const bool e0 = minL1 == EMIN, e1 = minL2 == EMIN;
+      if ((e0 && e1) || d >= gm.m + gm.n) {
+        if (t == 0) {
+          ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level; o.cells = cells; o.pad = 0;
+          P.ext[item] = o;
+        }
+        active = false;
+        break;
+      }
+      int qmn = 1 << 30, qmx = -(1 << 30);
+      if (!e0) { qmn = 2 * minL1 - d - K0; qmx = 2 * maxL1 - d - K0; }
+      if (!e1) { qmn = min(qmn, 2 * minL2 - (d - 1) - K0); qmx = max(qmx, 2 * maxL2 - (d - 1) - K0); }
+      int dir = 0;
+      if (qmx >= 2 * S - 2) dir = qmn >= 4 ? 1 : 2;
+      else if (qmn <= 1) dir = qmx <= 2 * S - 5 ? -1 : 2;
+      if (dir == 2) {                              // wider than the block window: restart unbounded
+        if (t == 0) push_item(esc.fb_items, esc.fb_tail, item);
+        active = false;
+        break;
+      }
+      if (dir != 0) {
+        // shift by 2 diagonals across the block: R[r] <- R[r + 2 dir]
+        int n0, n1;
+        if (dir > 0) {
+          if (lane == 0) { sh_next[w][0] = R[0]; sh_next[w][1] = R[1]; }
+          __syncthreads();
+          n0 = __shfl_down_sync(FULL, R[0], 1); n1 = __shfl_down_sync(FULL, R[1], 1);
+          if (lane == 31) { n0 = w < NW - 1 ? sh_next[w + 1][0] : NEGV; n1 = w < NW - 1 ? sh_next[w + 1][1] : NEGV; }
+#pragma unroll
+          for (int r = 0; r < NR - 2; ++r) R[r] = R[r + 2];
+          R[NR - 2] = n0; R[NR - 1] = n1;
+        } else {
+          if (lane == 31) { sh_next[w][0] = R[NR - 2]; sh_next[w][1] = R[NR - 1]; }
+          __syncthreads();
+          n0 = __shfl_up_sync(FULL, R[NR - 2], 1); n1 = __shfl_up_sync(FULL, R[NR - 1], 1);
+          if (lane == 0) { n0 = w > 0 ? sh_next[w - 1][0] : NEGV; n1 = w > 0 ? sh_next[w - 1][1] : NEGV; }
+#pragma unroll
+          for (int r = NR - 1; r >= 2; --r) R[r] = R[r - 2];
+          R[0] = n0; R[1] = n1;
+        }
+        K0 += 2 * dir; ia0 += dir; jb0 -= dir;
+        reload();
+        // refresh the edges of the current buffer (read by the next anti-diagonal)
+        if (lane == 0) edgeL[d & 1][w] = R[0];
+        if (lane == 31) edgeR[d & 1][w] = R[NR - 1];
+        __syncthreads();
+      }
+    }
+    __syncthreads();
   }
 }
 

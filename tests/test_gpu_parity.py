@@ -79,16 +79,29 @@ def test_unrelated_wide_bands_escalate(xd):
     assert st["escalated"][0] > 0
 
 
-def test_general_path_huge_band(xd):
-    """X large enough that nothing is pruned: band > 1024 -> general kernel."""
+def test_cta_path_wide_band(xd):
+    """X large enough that nothing is pruned, hull 1000-3000 cells: checkpoints travel
+    lane -> lane pair -> warp (256) -> warp (1024) -> CTA (4096) and resume exactly."""
     from synth import workload as W
-    w = W.random_pairs_workload(seed=9, n_pairs=6, len_lo=1200, len_hi=1500, k=5, X=100000, related=0.0)
+    w = W.random_pairs_workload(seed=9, n_pairs=8, len_lo=1200, len_hi=3000, k=5, X=100000, related=0.0)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=5, X=100000)
+        st = al.stats()
+    ref, rcells = oracle_of(w, X=100000)
+    assert_same(res, cells, ref, rcells, "cta")
+    assert st["escalated"][2] > 0 and st["escalated"][3] == 0
+
+
+def test_general_path_huge_band(xd):
+    """Hull wider than the CTA window (4096 cells): the unbounded kernel restarts it."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=19, n_pairs=3, len_lo=4500, len_hi=5000, k=5, X=100000, related=0.0)
     with xd.Aligner() as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=5, X=100000)
         st = al.stats()
     ref, rcells = oracle_of(w, X=100000)
     assert_same(res, cells, ref, rcells, "general")
-    assert st["escalated"][2] > 0
+    assert st["escalated"][3] > 0
 
 
 def test_ecoli_shaped_sample_full_launch(xd):

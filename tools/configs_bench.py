@@ -40,7 +40,7 @@ def run(al, w, X=None, reps=3):
 def fmt_row(name, w, X, r, c, st, wall):
     ms = st["total_ms"]
     return (f"| {name} | {w.n_pairs} | {X} | {c.sum():.3e} | {ms:.2f} | {c.sum() / ms / 1e6:.1f} | "
-            f"{w.n_pairs / ms * 1e3:.3e} | {st['level_ms'][0]:.2f} | {st['escalated'][:3]} | {st['long_items']} | "
+            f"{w.n_pairs / ms * 1e3:.3e} | {'/'.join('%.1f' % x for x in st['level_ms'])} | {st['escalated']} | {st['long_items']} | "
             f"{wall * 1e3:.1f} |")
 
 
@@ -49,31 +49,39 @@ def main():
     ap.add_argument("--celegans-scale", type=float, default=0.05)
     ap.add_argument("--logical-devices", type=int, default=4)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="comma list of: cfg1,ecoli,xsweep,celegans,policies")
     args = ap.parse_args()
-    lines = ["| config | pairs | X | cells | device ms (pipeline) | GCUPS | alignments/s | band kernel ms | "
-             "escalated (l1,l2,gen) | long-mode ext. | host-API wall ms (incl. H2D/D2H) |",
+    lines = ["| config | pairs | X | cells | device ms (pipeline) | GCUPS | alignments/s | tier ms (T0-2 / S1024 / - / unbounded) | "
+             "checkpoints (T0>T1, T1>T2, T2>S1024, unbounded restarts) | long-mode ext. | host-API wall ms (incl. H2D/D2H) |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
+    only = set(args.only.split(",")) if args.only else {"cfg1", "ecoli", "xsweep", "celegans", "policies"}
     al = xd.Aligner()
-    for name in ["cfg1", "ecoli"]:
+    nonmono, w5, gen_s, wx = None, None, 0.0, None
+    for name in [n for n in ["cfg1", "ecoli"] if n in only]:
         w = W.config(name)
         lines.append(fmt_row(name, w, w.X, *run(al, w)))
         print(lines[-1], flush=True)
     # config 4: X sweep
-    wx = W.config("xsweep")
-    scores = {}
-    for X in (15, 50, 100):
-        r, c, st, wall = run(al, wx, X=X, reps=2)
-        scores[X] = r["score"].copy()
-        lines.append(fmt_row("xsweep", wx, X, r, c, st, wall))
-        print(lines[-1], flush=True)
-    nonmono = int(np.sum((scores[50] < scores[15]) | (scores[100] < scores[50])))
+    if "xsweep" in only:
+        wx = W.config("xsweep")
+        scores = {}
+        for X in (15, 50, 100):
+            r, c, st, wall = run(al, wx, X=X, reps=2)
+            scores[X] = r["score"].copy()
+            lines.append(fmt_row("xsweep", wx, X, r, c, st, wall))
+            print(lines[-1], flush=True)
+        nonmono = int(np.sum((scores[50] < scores[15]) | (scores[100] < scores[50])))
     # config 5
-    t = time.perf_counter()
-    w5 = W.config("celegans", scale=args.celegans_scale)
-    gen_s = time.perf_counter() - t
-    lines.append(fmt_row(f"celegans x{args.celegans_scale}", w5, w5.X, *run(al, w5, reps=2)))
-    print(lines[-1], flush=True)
+    if "celegans" in only:
+        t = time.perf_counter()
+        w5 = W.config("celegans", scale=args.celegans_scale)
+        gen_s = time.perf_counter() - t
+        lines.append(fmt_row(f"celegans x{args.celegans_scale}", w5, w5.X, *run(al, w5, reps=2)))
+        print(lines[-1], flush=True)
     al.close()
+    if "policies" not in only:
+        print("\n".join(lines))
+        return
     # config 3: the paper's policies on logical devices
     w = W.config("ecoli")
     m = args.logical_devices
@@ -96,10 +104,10 @@ def main():
     import torch
     gpu = torch.cuda.get_device_name(0)
     text = "\n".join([f"# Configs on {gpu} (1 physical GPU)", "", "## Throughput", ""] + lines + [
-        "", f"X-sweep pairs whose score is NOT monotone in X (15 -> 50 -> 100): {nonmono} of {wx.n_pairs}",
+        "", f"X-sweep pairs whose score is NOT monotone in X (15 -> 50 -> 100): {nonmono} of {wx.n_pairs if wx else 0}",
         f"(DESIGN.md Q25: monotonicity is not a property of X-drop).", "",
         f"config 5 generated at scale {args.celegans_scale} in {gen_s:.1f} s "
-        f"({w5.n_pairs} pairs, {len(w5.offsets) - 1} reads).", "",
+        f"({w5.n_pairs if w5 else 0} pairs, {len(w5.offsets) - 1 if w5 else 0} reads).", "",
         f"## Config 3 analog: the paper's policies, 16 logical ranks over {m} logical devices", "",
         "Logical devices are streams of one B200, so spans show policy overheads and serialisation, not",
         "multi-GPU scaling. Results are identical for every policy (asserted).", ""] + pol) + "\n"
