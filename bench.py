@@ -18,6 +18,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import subprocess
 import sys
 import tempfile
@@ -112,9 +113,11 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "25"],
-                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            cmd = ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                   "-lms", "50"]
+            if shutil.which("stdbuf"):             # line-buffered, or samples are lost on terminate
+                cmd = ["stdbuf", "-oL"] + cmd
+            self.proc = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -226,16 +229,15 @@ def run_native(args, world, rank, local):
     def step():
         al.align_device(seq_d, off_d, pairs_d, out_d, cells_d, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g, stream=stream)
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize(dev)
-    cells_step = int(cells_d.sum().item())
-
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     step_ms, l0_ms, stats = [], [], []
-    barrier(world)
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:          # clocks over warm-up + timed steps (same load)
+        for _ in range(max(3, args.warmup)):
+            step()
+        torch.cuda.synchronize(dev)
+        cells_step = int(cells_d.sum().item())
+        barrier(world)
+        torch.cuda.synchronize(dev)
         for i in range(args.steps):
             flush.zero_()                                   # untimed L2 flush between timed steps
             ev[i][0].record(stream)

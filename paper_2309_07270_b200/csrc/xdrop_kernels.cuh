@@ -202,10 +202,11 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
     }
   }
   const int two = keym >> (KEYSH - 1);  // 2, opaque: keeps ch * two + s an IMAD
-  int key[C];
+  int kacc[NCH];                        // running argmax keys, one per chain (max3 of pairs)
+  int kpend[NCH];                       // a key waiting for its partner
   int ch[NCH];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) ch[c] = 0;
+  for (int c = 0; c < NCH; ++c) { ch[c] = 0; kacc[c] = NEGV * 128; kpend[c] = NEGV * 128; }
 #pragma unroll
   for (int tt = 0; tt < C; ++tt) {
     const int r = 2 * tt + PAR;
@@ -223,13 +224,21 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
     }
     v = v | (sd & (int)0xFF800000);
     B.R[r] = v;
-    key[tt] = v * keym + (127 - tt);
+    const int key = v * keym + (127 - tt);
+    if ((tt % CL) % 2 == 0) kpend[tt / CL] = key;
+    else kacc[tt / CL] = __vimax3_s32(kacc[tt / CL], kpend[tt / CL], key);
     ch[tt / CL] = ch[tt / CL] * two + sd;  // accumulates -(dead bits)
   }
   unsigned dbits = 0;                   // cell tt at bit C-1-tt
 #pragma unroll
   for (int c = 0; c < NCH; ++c) dbits = (dbits << CL) + (unsigned)(-ch[c]);
-  const int mk = tree_max3<C>(key);
+  int mk;
+  if constexpr (CL % 2 == 1) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) kacc[c] = max(kacc[c], kpend[c]);
+  }
+  if constexpr (NCH == 4) mk = max(__vimax3_s32(kacc[0], kacc[1], kacc[2]), kacc[3]);
+  else mk = kacc[0];
   // ---- critical path: next threshold
   const int vl = mk >> KEYSH;           // best W value of this lane (NEGV if none live)
   int gv, gt;
