@@ -1004,24 +1004,28 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
 // ----------------------------------------------------------- pack / prepare
 // ASCII -> 2-bit (A0 C1 G2 T3, base t at bits 2(t mod 16) of word t/16),
 // written at pool index + GUARD.  Any other byte sets *bad to its index.
+__device__ __forceinline__ uint32_t code_of(unsigned ch, int64_t t, unsigned long long* bad) {
+  const unsigned u = ch & 0xDFu;   // upper case
+  if (!(u == 'A' || u == 'C' || u == 'G' || u == 'T')) atomicMin(bad, (unsigned long long)t);
+  return ((ch >> 1) ^ (ch >> 2)) & 3u;   // A/a 0, C/c 1, G/g 2, T/t 3
+}
 __global__ void pack_kernel(const char* __restrict__ seq, int64_t len, uint32_t* __restrict__ out,
                             unsigned long long* bad) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // output word of the pool
   const int64_t nwords = (len + GUARD + 15) / 16;
   if (w >= nwords) return;
   uint32_t word = 0;
-  const int64_t t0 = w * 16 - GUARD;   // pool index of the first base in this word
+  const int64_t t0 = w * 16 - GUARD;   // pool index of the first base in this word (GUARD % 16 == 0)
+  if (t0 >= 0 && t0 + 16 <= len && ((reinterpret_cast<uintptr_t>(seq) & 15) == 0)) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(seq + t0));   // one 16-byte load
+    const uint32_t v[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int64_t t = t0 + u;
-    if (t >= 0 && t < len) {
-      const unsigned char ch = (unsigned char)seq[t];
-      const unsigned char c = ch & 0xDF;   // upper case
-      uint32_t code;
-      if (c == 'A') code = 0; else if (c == 'C') code = 1; else if (c == 'G') code = 2;
-      else if (c == 'T') code = 3;
-      else { code = 0; atomicMin(bad, (unsigned long long)t); }
-      word |= code << (2 * u);
+    for (int u = 0; u < 16; ++u) word |= code_of((v[u >> 2] >> (8 * (u & 3))) & 0xFFu, t0 + u, bad) << (2 * u);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int64_t t = t0 + u;
+      if (t >= 0 && t < len) word |= code_of((unsigned char)seq[t], t, bad) << (2 * u);
     }
   }
   out[w] = word;
@@ -1114,31 +1118,37 @@ __global__ void scatter_kernel(const int* __restrict__ wcost, int64_t n_items, i
 __global__ void combine_kernel(Problem P, int* __restrict__ out5, long long* __restrict__ cells_out,
                                unsigned long long* __restrict__ level_acc) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P.n_pairs) return;
-  const PairDesc pd = P.pairs[p];
-  const int64_t xa = P.offA[pd.a_id] + GUARD + pd.a_pos, xb = P.offB[pd.b_id] + GUARD + pd.b_pos;
-  int mism = 0;
-  for (int t = 0; t < P.k; t += 16) {
-    const uint32_t x = fwd16(P.PA, xa + t) ^ fwd16(P.PB, xb + t);
-    uint32_t f = (x | (x >> 1)) & 0x55555555u;
-    const int rem = P.k - t;
-    if (rem < 16) f &= (1u << (2 * rem)) - 1u;
-    mism += __popc(f);
+  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per-level [cells x4, items x4]
+  if (p < P.n_pairs) {
+    const PairDesc pd = P.pairs[p];
+    const int64_t xa = P.offA[pd.a_id] + GUARD + pd.a_pos, xb = P.offB[pd.b_id] + GUARD + pd.b_pos;
+    int mism = 0;
+    for (int t = 0; t < P.k; t += 16) {
+      const uint32_t x = fwd16(P.PA, xa + t) ^ fwd16(P.PB, xb + t);
+      uint32_t f = (x | (x >> 1)) & 0x55555555u;
+      const int rem = P.k - t;
+      if (rem < 16) f &= (1u << (2 * rem)) - 1u;
+      mism += __popc(f);
+    }
+    const int seed = (P.k - mism) * P.M + mism * P.mu;
+    const ExtOut L = P.ext[2 * p], R = P.ext[2 * p + 1];
+    int* o = out5 + 5 * p;
+    o[0] = L.best + seed + R.best;
+    o[1] = pd.a_pos - L.istar;
+    o[2] = pd.a_pos + P.k + R.istar;
+    o[3] = pd.b_pos - L.jstar;
+    o[4] = pd.b_pos + P.k + R.jstar;
+    if (cells_out) cells_out[p] = L.cells + R.cells;
+    acc[L.level & 3] += (unsigned long long)L.cells; acc[R.level & 3] += (unsigned long long)R.cells;
+    acc[4 + (L.level & 3)] += 1; acc[4 + (R.level & 3)] += 1;
   }
-  const int seed = (P.k - mism) * P.M + mism * P.mu;
-  const ExtOut L = P.ext[2 * p], R = P.ext[2 * p + 1];
-  int* o = out5 + 5 * p;
-  o[0] = L.best + seed + R.best;
-  o[1] = pd.a_pos - L.istar;
-  o[2] = pd.a_pos + P.k + R.istar;
-  o[3] = pd.b_pos - L.jstar;
-  o[4] = pd.b_pos + P.k + R.jstar;
-  if (cells_out) cells_out[p] = L.cells + R.cells;
-  // per-level accounting (stats): [cells x4, items x4]
-  atomicAdd(&level_acc[L.level & 3], (unsigned long long)L.cells);
-  atomicAdd(&level_acc[R.level & 3], (unsigned long long)R.cells);
-  atomicAdd(&level_acc[4 + (L.level & 3)], 1ull);
-  atomicAdd(&level_acc[4 + (R.level & 3)], 1ull);
+  // reduce per warp (every lane reaches here), one atomic per counter per warp
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long v = acc[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&level_acc[i], v);
+  }
 }
 
 // ----------------------------------------------------- INT32 issue-rate probe
