@@ -98,10 +98,14 @@ typedef struct {
   int64_t n;              /* number of reads */
 } xdrop_seqs;
 
-/* One candidate pair: seed A[a_pos, a_pos+k) ~ B[b_pos, b_pos+k).  16 bytes. */
+/* One candidate pair: seed A[a_pos, a_pos+k) ~ B'[b_pos, b_pos+k).  16 bytes.
+ * B' = B, or reverse(complement(B)) when b_id has bit 31 set (b_id | XDROP_PAIR_RC: the
+ * reads come from opposite strands); b_pos, b_begin and b_end are then positions in B'
+ * (reading Q16). */
 typedef struct {
   int32_t a_id, b_id, a_pos, b_pos;
 } xdrop_pair;
+#define XDROP_PAIR_RC ((int32_t)0x80000000)
 
 /* Result of ALIGN, 0-based half-open coordinates [begin, end).  20 bytes. */
 typedef struct {

@@ -68,6 +68,17 @@ typedef struct {
 
 static int up(int c) { return (c >= 'a' && c <= 'z') ? c - 32 : c; }
 
+/* Watson-Crick complement of a base (reading Q16: strand) */
+static unsigned char complement(unsigned char c) {
+  switch (up(c)) {
+    case 'A': return 'T';
+    case 'C': return 'G';
+    case 'G': return 'C';
+    case 'T': return 'A';
+    default: return c;
+  }
+}
+
 /* s(x,y) = M if x == y (case-insensitive), else mu  (reading Q10) */
 static int sub_score(unsigned char x, unsigned char y, int M, int mu) {
   return up(x) == up(y) ? M : mu;
@@ -221,11 +232,19 @@ static void *worker(void *arg) {
     const int32_t *q = B->pairs + 4 * p;
     const unsigned char *A = B->seqA + B->offA[q[0]];
     int64_t lenA = B->offA[q[0] + 1] - B->offA[q[0]];
-    const unsigned char *Bs = B->seqB + B->offB[q[1]];
-    int64_t lenB = B->offB[q[1] + 1] - B->offB[q[1]];
+    const int32_t bid = q[1] & 0x7fffffff;               /* bit 31: use reverse(complement(B)) */
+    const unsigned char *Bs = B->seqB + B->offB[bid];
+    int64_t lenB = B->offB[bid + 1] - B->offB[bid];
+    unsigned char *rcb = NULL;
+    if (q[1] & (int32_t)0x80000000) {
+      rcb = (unsigned char *)malloc((size_t)lenB + 1);
+      for (int64_t u = 0; u < lenB; ++u) rcb[u] = complement(Bs[lenB - 1 - u]);
+      Bs = rcb;
+    }
     int64_t c = 0;
     int rc = oracle_align(A, lenA, Bs, lenB, q[2], q[3], B->k, B->M, B->mu, B->g, B->X,
                           &B->out[p], &c, NULL, NULL);
+    free(rcb);
     if (B->cells) B->cells[p] = c;
     if (rc) {
       pthread_mutex_lock(&B->mu_lock);

@@ -82,8 +82,17 @@ def fulldp(a: str, b: str, M=1, mu=-1, g=-1):
     return best
 
 
-def align(A: str, B: str, a_pos: int, b_pos: int, k: int, M=1, mu=-1, g=-1, X=15):
-    """ALIGN (reading Q9, Q13): seed columns + right EXTEND + left EXTEND on reversals."""
+def revcomp(B: str) -> str:
+    """Reverse complement (reading Q16: a pair may use B on the other strand)."""
+    comp = {"A": "T", "C": "G", "G": "C", "T": "A"}
+    return "".join(comp[c.upper()] for c in reversed(B))
+
+
+def align(A: str, B: str, a_pos: int, b_pos: int, k: int, M=1, mu=-1, g=-1, X=15, rc=False):
+    """ALIGN (reading Q9, Q13): seed columns + right EXTEND + left EXTEND on reversals.
+    rc=True aligns A against revcomp(B); b_pos / b_begin / b_end are revcomp(B) coordinates."""
+    if rc:
+        B = revcomp(B)
     seed = sum(s(A[a_pos + t], B[b_pos + t], M, mu) for t in range(k))
     R = extend(A[a_pos + k:], B[b_pos + k:], M, mu, g, X)
     L = extend(A[:a_pos][::-1], B[:b_pos][::-1], M, mu, g, X)

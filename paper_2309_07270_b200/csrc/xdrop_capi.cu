@@ -576,9 +576,10 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   // seeds and ids (a2), reported with the offending pair index
   for (int64_t t = 0; t < n_pairs; ++t) {
     const xdrop_pair& q = pairs[t];
-    if (q.a_id < 0 || q.a_id >= A->n || q.b_id < 0 || q.b_id >= B->n) { ctx->err_index = t; return XDROP_EINVAL; }
+    const int32_t bid = q.b_id & 0x7fffffff;   // bit 31 = XDROP_PAIR_RC
+    if (q.a_id < 0 || q.a_id >= A->n || bid >= B->n) { ctx->err_index = t; return XDROP_EINVAL; }
     const int64_t la = A->offsets[q.a_id + 1] - A->offsets[q.a_id];
-    const int64_t lb = B->offsets[q.b_id + 1] - B->offsets[q.b_id];
+    const int64_t lb = B->offsets[bid + 1] - B->offsets[bid];
     if (q.a_pos < 0 || q.b_pos < 0 || q.a_pos + (int64_t)p->k > la || q.b_pos + (int64_t)p->k > lb) {
       ctx->err_index = t;
       return XDROP_ESEED;
@@ -606,8 +607,9 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   std::vector<int64_t> w((size_t)n_pairs);
   for (int64_t t = 0; t < n_pairs; ++t) {
     const xdrop_pair& q = pairs[t];
+    const int32_t bid = q.b_id & 0x7fffffff;
     const int64_t la = A->offsets[q.a_id + 1] - A->offsets[q.a_id];
-    const int64_t lb = B->offsets[q.b_id + 1] - B->offsets[q.b_id];
+    const int64_t lb = B->offsets[bid + 1] - B->offsets[bid];
     w[(size_t)t] = std::min<int64_t>(q.a_pos, q.b_pos) + std::min<int64_t>(la - q.a_pos - p->k, lb - q.b_pos - p->k) + 1;
   }
   xdrop_sched_cfg cfg{m, ctx->opts.policy, ctx->opts.n_ranks, ctx->opts.batch_size, ctx->opts.subbatches};

@@ -62,11 +62,14 @@ __device__ __forceinline__ uint32_t fwd16(const uint32_t* __restrict__ P, int64_
   const uint32_t lo = __ldg(P + w), hi = __ldg(P + w + 1);
   return __funnelshift_r(lo, hi, sh);
 }
-// chars t .. t+15 of a stream (start, dir); dir < 0 reads backwards and
-// returns codes with their two bits swapped -- harmless, both streams of an
-// extension share the direction, and only equality of codes is used.
+// swap the two bits of every 2-bit field (undoes __brev's per-field bit reversal)
+__device__ __forceinline__ uint32_t swap_pairs(uint32_t y) {
+  return ((y >> 1) & 0x55555555u) | ((y & 0x55555555u) << 1);
+}
+// chars t .. t+15 of a stream (start, dir) as true 2-bit codes; dir < 0 reads backwards
+// (the two streams of an RC pair run in opposite directions, so codes must be exact)
 __device__ __forceinline__ uint32_t load16(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
-  return dir > 0 ? fwd16(P, start + t) : __brev(fwd16(P, start - t - 15));
+  return dir > 0 ? fwd16(P, start + t) : swap_pairs(__brev(fwd16(P, start - t - 15)));
 }
 __device__ __forceinline__ uint64_t load32c(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
   return (uint64_t)load16(P, start, dir, t) | ((uint64_t)load16(P, start, dir, t + 16) << 32);
@@ -81,21 +84,32 @@ __device__ __forceinline__ int char_at(const uint32_t* __restrict__ P, int64_t s
   return (int)((__ldg(P + (x >> 4)) >> ((int)(x & 15) << 1)) & 3u);
 }
 
-struct Geom { int64_t sa, sb; int da, db; int m, n; };
+// b_id bit 31 (XDROP_PAIR_RC): the pair uses reverse(complement(B)); b_pos and the
+// reported B coordinates are positions in revcomp(B) (reading Q16)
+constexpr int32_t PAIR_RC = (int32_t)0x80000000;
+
+struct Geom { int64_t sa, sb; int da, db; int m, n; uint64_t bmask; };
 
 __device__ __forceinline__ Geom item_geom(const Problem& P, int item) {
   const int p = item >> 1;
   const PairDesc pd = P.pairs[p];
-  const int64_t a0 = P.offA[pd.a_id] + GUARD, b0 = P.offB[pd.b_id] + GUARD;
+  const bool rc = (pd.b_id & PAIR_RC) != 0;
+  const int bid = pd.b_id & 0x7fffffff;
+  const int64_t a0 = P.offA[pd.a_id] + GUARD, b0 = P.offB[bid] + GUARD;
   const int lenA = (int)(P.offA[pd.a_id + 1] - P.offA[pd.a_id]);
-  const int lenB = (int)(P.offB[pd.b_id + 1] - P.offB[pd.b_id]);
+  const int lenB = (int)(P.offB[bid + 1] - P.offB[bid]);
   Geom G;
-  if (item & 1) {   // right extension: A[a_pos+k:], B[b_pos+k:]
+  G.bmask = rc ? ~0ull : 0ull;       // complemented codes: XOR every field with 3
+  if (item & 1) {   // right extension: A[a_pos+k:], B'[b_pos+k:]
     G.sa = a0 + pd.a_pos + P.k; G.da = 1; G.m = lenA - pd.a_pos - P.k;
-    G.sb = b0 + pd.b_pos + P.k; G.db = 1; G.n = lenB - pd.b_pos - P.k;
-  } else {          // left extension: reverse(A[:a_pos]), reverse(B[:b_pos])
+    G.n = lenB - pd.b_pos - P.k;
+    if (!rc) { G.sb = b0 + pd.b_pos + P.k; G.db = 1; }
+    else { G.sb = b0 + lenB - 1 - pd.b_pos - P.k; G.db = -1; }   // B'[t] = comp(B[lenB-1-t])
+  } else {          // left extension: reverse(A[:a_pos]), reverse(B'[:b_pos])
     G.sa = a0 + pd.a_pos - 1; G.da = -1; G.m = pd.a_pos;
-    G.sb = b0 + pd.b_pos - 1; G.db = -1; G.n = pd.b_pos;
+    G.n = pd.b_pos;
+    if (!rc) { G.sb = b0 + pd.b_pos - 1; G.db = -1; }
+    else { G.sb = b0 + lenB - pd.b_pos; G.db = 1; }
   }
   return G;
 }
@@ -146,6 +160,7 @@ __device__ __forceinline__ int tree_max3(int (&k)[N]) {
 template <int C> struct Band {
   int R[2 * C];                 // diagonals K0 + 2C*gl + r, r in [0, 2C)
   uint64_t Aw, Bw;              // a[ia0_l + t], b[jb0_l - t] for t = 0..31
+  uint64_t bmask;               // ~0 when b is complemented (reverse-complement pairs)
   uint32_t An, An2, Bn, Bn2;    // stream reservoirs (next chars in stream order)
   int64_t sa, sb; int da, db;
   int m, n, K0, ia0, jb0;       // ia0/jb0: char index of global cell t = 0
@@ -190,7 +205,7 @@ __device__ __forceinline__ void band_diag(Band<C>& B, int gl, int d, int qlo, in
   const int thr = B.thrW;
   const int M = P.M - 2 * P.g, mu = P.mu - 2 * P.g;
   const int keym = P.keym;
-  const uint64_t x = B.Aw ^ B.Bw;
+  const uint64_t x = B.Aw ^ B.Bw ^ B.bmask;
   int nb = NEGV;
   if constexpr (G > 1) {
     if constexpr (PAR == 0) {
@@ -497,7 +512,7 @@ __device__ __forceinline__ void band_loop(Band<C>& B, int gl, int& d, int& rem, 
 template <int C>
 __device__ __forceinline__ void band_idle(Band<C>& B) {
   B.active = false; B.item = 0;
-  B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0;
+  B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0; B.bmask = 0;
 }
 
 // Run one extension from its seed per group of G lanes (item < 0: idle group).  Warp-collective.
@@ -509,7 +524,7 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
   if (item >= 0) {
     B.active = true; B.item = item;
     const Geom gm = item_geom(P, B.item);
-    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n; B.bmask = gm.bmask;
   } else {
     band_idle(B);
   }
@@ -548,7 +563,7 @@ __device__ __forceinline__ void band_resume(const Problem& P, const int* rec, in
   if (rec) {
     B.active = true; B.item = rec[0];
     const Geom gm = item_geom(P, B.item);
-    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n; B.bmask = gm.bmask;
     d = rec[1];
     const int s_src = rec[14];
     const int sh = S - s_src;                      // K0' = K0 - sh (sh >= 0, even)
@@ -800,7 +815,7 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
         const int pb = (d - 1) & 1, cb = d & 1;      // previous / current buffers
         const int M2 = P.M - 2 * P.g, mu2 = P.mu - 2 * P.g;
         const int qlo = d - K0 - 2 * gm.n, qhi = 2 * gm.m - d - K0;
-        const uint64_t x = Aw ^ Bw;
+        const uint64_t x = Aw ^ Bw ^ gm.bmask;
         int nb;
         if (par == 0) { nb = __shfl_up_sync(FULL, R[NR - 1], 1); if (lane == 0) nb = w > 0 ? edgeR[pb][w - 1] : NEGV; }
         else { nb = __shfl_down_sync(FULL, R[0], 1); if (lane == 31) nb = w < NW - 1 ? edgeL[pb][w + 1] : NEGV; }
@@ -973,7 +988,7 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
         if (j >= 1 && i >= lo_[p1] && i <= hi_[p1]) v = max(v, H[p1][i] + P.g);
         if (i >= 1 && j >= 1 && i - 1 >= lo_[p2] && i - 1 <= hi_[p2]) {
           const int ca = char_at(P.PA, gm.sa, gm.da, i - 1);
-          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1);
+          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1) ^ (int)(gm.bmask & 3ull);
           v = max(v, H[p2][i - 1] + (ca == cb ? P.M : P.mu));
         }
         const bool live = v >= thr;
@@ -1037,11 +1052,12 @@ __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict_
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P.n_pairs) return;
   const PairDesc pd = P.pairs[p];
-  bool ok = pd.a_id >= 0 && pd.a_id < P.nA && pd.b_id >= 0 && pd.b_id < P.nB;
+  const int bid = pd.b_id & 0x7fffffff;
+  bool ok = pd.a_id >= 0 && pd.a_id < P.nA && bid < P.nB;
   int wl = 0, wr = 0;
   if (ok) {
     const int64_t lenA = P.offA[pd.a_id + 1] - P.offA[pd.a_id];
-    const int64_t lenB = P.offB[pd.b_id + 1] - P.offB[pd.b_id];
+    const int64_t lenB = P.offB[bid + 1] - P.offB[bid];
     ok = pd.a_pos >= 0 && pd.b_pos >= 0 && pd.a_pos + (int64_t)P.k <= lenA &&
          pd.b_pos + (int64_t)P.k <= lenB && lenA <= max_len && lenB <= max_len;
     if (ok) {
@@ -1121,10 +1137,16 @@ __global__ void combine_kernel(Problem P, int* __restrict__ out5, long long* __r
   unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per-level [cells x4, items x4]
   if (p < P.n_pairs) {
     const PairDesc pd = P.pairs[p];
-    const int64_t xa = P.offA[pd.a_id] + GUARD + pd.a_pos, xb = P.offB[pd.b_id] + GUARD + pd.b_pos;
+    const bool rc = (pd.b_id & PAIR_RC) != 0;
+    const int bid = pd.b_id & 0x7fffffff;
+    const int64_t xa = P.offA[pd.a_id] + GUARD + pd.a_pos;
+    const int64_t lenB = P.offB[bid + 1] - P.offB[bid];
+    // seed columns of B' = B (forward) or revcomp(B) (backward, complemented)
+    const int64_t xb = P.offB[bid] + GUARD + (rc ? lenB - 1 - pd.b_pos : pd.b_pos);
     int mism = 0;
     for (int t = 0; t < P.k; t += 16) {
-      const uint32_t x = fwd16(P.PA, xa + t) ^ fwd16(P.PB, xb + t);
+      const uint32_t bw = rc ? ~load16(P.PB, xb, -1, t) : fwd16(P.PB, xb + t);
+      const uint32_t x = fwd16(P.PA, xa + t) ^ bw;
       uint32_t f = (x | (x >> 1)) & 0x55555555u;
       const int rem = P.k - t;
       if (rem < 16) f &= (1u << (2 * rem)) - 1u;

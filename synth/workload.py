@@ -122,8 +122,10 @@ def _choose_seed(rng, sa, ca, sb, cb, k):
 def make_pool_workload(name: str, seed: int, genome_len: int, n_pairs: int, length_sampler,
                        coverage: float, min_ov: int, k: int = 17, X: int = 15,
                        sub: float = 0.015, ins: float = 0.09, dele: float = 0.045,
-                       f_sp: float = 0.0, max_reads: Optional[int] = None) -> Workload:
-    """Pool mode: reads from one genome; pairs are overlapping reads (plus spurious)."""
+                       f_sp: float = 0.0, max_reads: Optional[int] = None, rc_frac: float = 0.0) -> Workload:
+    """Pool mode: reads from one genome; pairs are overlapping reads (plus spurious).
+    rc_frac: fraction of reads sequenced from the reverse strand (stored reverse-
+    complemented); pairs of reads from opposite strands carry XDROP_PAIR_RC."""
     rng = np.random.default_rng(seed)
     genome = rng.integers(0, 4, size=genome_len, dtype=np.uint8)
     mean_len = float(np.mean(length_sampler(rng, 4096)))
@@ -179,12 +181,29 @@ def make_pool_workload(name: str, seed: int, genome_len: int, n_pairs: int, leng
         reads.append(copy)
         extra.append((i, len(reads) - 1, pa, pb))
     allp = pairs + extra
+    if rc_frac > 0:
+        # store a fraction of reads reverse-complemented and re-express every pair in stored coordinates
+        flip = rng.random(len(reads)) < rc_frac
+        lens = [r.shape[0] for r in reads]
+        out = []
+        for (i, j, pa, pb) in allp:
+            fi, fj = bool(flip[i]), bool(flip[j])
+            if fi and fj:                   # both reversed: an ordinary pair on the stored strand
+                out.append((i, j, lens[i] - pa - k, lens[j] - pb - k))
+            elif fj:                        # B reversed: revcomp(stored B) == forward B
+                out.append((i, j | PAIR_RC, pa, pb))
+            elif fi:                        # A reversed: swap roles, B = stored A taken reverse-complemented
+                out.append((j, i | PAIR_RC, pb, pa))
+            else:
+                out.append((i, j, pa, pb))
+        allp = out
+        reads = [revcomp_codes(r) if flip[t] else r for t, r in enumerate(reads)]
     order = rng.permutation(len(allp))
     seq, off = _pack_pool(reads)
     arr = np.array(allp, dtype=np.int32).reshape(-1, 4)[order] if allp else np.zeros((0, 4), np.int32)
     recipe = dict(mode="pool", seed=seed, genome_len=genome_len, n_reads=len(reads),
                   coverage=coverage, min_ov=min_ov, k=k, X=X, sub=sub, ins=ins, dele=dele,
-                  f_sp=f_sp, n_pairs=int(arr.shape[0]), mean_read_len=float(np.mean(lengths)))
+                  f_sp=f_sp, rc_frac=rc_frac, n_pairs=int(arr.shape[0]), mean_read_len=float(np.mean(lengths)))
     return Workload(name, seq, off, np.ascontiguousarray(arr), k, X, recipe=recipe)
 
 
@@ -277,9 +296,19 @@ def config(name: str, scale: float = 1.0, X: Optional[int] = None, seed: Optiona
     return w
 
 
+PAIR_RC = -(1 << 31)          # bit 31 of b_id (include/xdrop.h XDROP_PAIR_RC)
+
+
+def revcomp_codes(c: np.ndarray) -> np.ndarray:
+    """Reverse complement of 2-bit codes A0 C1 G2 T3 (complement = 3 - code)."""
+    return (3 - c[::-1]).astype(np.uint8)
+
+
 def random_pairs_workload(seed: int, n_pairs: int, len_lo: int, len_hi: int, k: int, X: int,
-                          M=1, mu=-1, g=-1, related=0.7, err=0.15) -> Workload:
-    """Unstructured random pairs for parity edge cases (ragged lengths, seeds at ends)."""
+                          M=1, mu=-1, g=-1, related=0.7, err=0.15, rc_frac=0.0) -> Workload:
+    """Unstructured random pairs for parity edge cases (ragged lengths, seeds at ends).
+    With rc_frac > 0 a fraction of pairs store B reverse-complemented and carry the
+    XDROP_PAIR_RC flag, so that A aligns against revcomp(stored B)."""
     rng = np.random.default_rng(seed)
     reads, pairs = [], []
     for p in range(n_pairs):
@@ -308,8 +337,12 @@ def random_pairs_workload(seed: int, n_pairs: int, len_lo: int, len_hi: int, k: 
             pb = int(rng.integers(0, b.shape[0] - k + 1))
         if rng.random() < 0.8:                       # make the seed exact
             b = b.copy(); b[pb:pb + k] = a[pa:pa + k]
+        bid = 2 * p + 1
+        if rc_frac and rng.random() < rc_frac:       # other strand: store revcomp(b), flag the pair
+            b = revcomp_codes(b)
+            bid |= PAIR_RC
         reads += [a, b]
-        pairs.append((2 * p, 2 * p + 1, pa, pb))
+        pairs.append((2 * p, bid, pa, pb))
     seq, off = _pack_pool(reads)
     return Workload(f"random{seed}", seq, off, np.array(pairs, dtype=np.int32).reshape(-1, 4), k, X, M, mu, g,
                     recipe=dict(mode="random", seed=seed, len_lo=len_lo, len_hi=len_hi, related=related))

@@ -212,3 +212,25 @@ def test_long_mode_multilane(xd, long_g, X, monkeypatch):
     assert_same(res, cells, ref, rcells, f"long G={long_g} X={X}")
     if long_g != "0":
         assert st["long_items"] > 0
+
+
+@pytest.mark.parametrize("X", [0, 5, 15, 60])
+def test_reverse_complement_pairs(xd, X):
+    """Strand (f2): XDROP_PAIR_RC pairs, mixed with forward pairs, every tier."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=400 + X, n_pairs=160, len_lo=0, len_hi=1500, k=13, X=X, rc_frac=0.5)
+    assert (w.pairs[:, 1] < 0).sum() > 40
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
+    ref, rcells = oracle_of(w, X=X)
+    assert_same(res, cells, ref, rcells, f"rc X={X}")
+
+
+def test_reverse_complement_pool_workload(xd):
+    from synth import workload as W
+    w = W.make_pool_workload("rc-pool", 77, 300_000, 400, W._normal_len(3000, 400, 1000, 6000), 10.0, 500,
+                             k=17, X=15, rc_frac=0.5, f_sp=0.05)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=17, X=15)
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, "rc pool")

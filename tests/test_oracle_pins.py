@@ -281,3 +281,49 @@ def test_batch_reports_bad_seed():
     off = np.array([0, 8], dtype=np.int64)
     with pytest.raises(ValueError):
         oracle.align_batch(seq, off, seq, off, np.array([[0, 0, 5, 0]]), 5)
+
+
+# ------------------------------------------------------------ strand (f2)
+def _rc(s):
+    return s.translate(str.maketrans("ACGT", "TGCA"))[::-1]
+
+
+def test_rc_pairs_closed_form_and_equivalence():
+    """Reading Q16: a pair with XDROP_PAIR_RC aligns A against revcomp(B), B coordinates in
+    revcomp(B).  Pinned by (1) B = revcomp(A) behaving exactly like identical reads (closed
+    form), (2) equality with the same pair written forward on an explicitly reverse-
+    complemented pool (a different input path through the oracle)."""
+    import numpy as np
+    rng = random.Random(29)
+    reads, pairs_rc, pairs_fw, fw_reads = [], [], [], []
+    for p in range(40):
+        A = "".join(rng.choice(ALPH) for _ in range(rng.randint(30, 150)))
+        Bf = mutate(rng, A, 0.15) if p % 2 else A        # forward-strand partner
+        if len(Bf) < 6:
+            Bf = A
+        pa = rng.randint(0, len(A) - 5)
+        pb = rng.randint(0, len(Bf) - 5)
+        Bs = _rc(Bf)                                     # stored on the other strand
+        reads += [A, Bs]
+        fw_reads += [A, Bf]
+        pairs_rc.append((2 * p, (2 * p + 1) | -(1 << 31), pa, pb))
+        pairs_fw.append((2 * p, 2 * p + 1, pa, pb))
+        if p % 2 == 0:                                   # B = revcomp(A): identical after RC
+            r = oracle.align_batch(np.frombuffer((A + Bs).encode(), np.uint8),
+                                   np.array([0, len(A), len(A) + len(Bs)]), np.frombuffer((A + Bs).encode(), np.uint8),
+                                   np.array([0, len(A), len(A) + len(Bs)]),
+                                   np.array([[0, 1 | -(1 << 31), pa, pa]]), 5, X=7)[0][0]
+            assert (r["score"], r["a_begin"], r["a_end"], r["b_begin"], r["b_end"]) == (len(A), 0, len(A), 0, len(A))
+
+    def pool(rs):
+        off = np.zeros(len(rs) + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in rs])
+        return np.frombuffer("".join(rs).encode(), np.uint8), off
+    s1, o1 = pool(reads)
+    s2, o2 = pool(fw_reads)
+    r1, c1 = oracle.align_batch(s1, o1, s1, o1, np.array(pairs_rc), 5, X=9)
+    r2, c2 = oracle.align_batch(s2, o2, s2, o2, np.array(pairs_fw), 5, X=9)
+    assert np.array_equal(r1, r2) and np.array_equal(c1, c2)
+    for t, (a, b, pa, pb) in enumerate(pairs_rc):         # and the Python twin
+        p = ref.align(reads[a], reads[b & 0x7fffffff], pa, pb, 5, X=9, rc=True)
+        assert (r1[t]["score"], r1[t]["b_begin"], r1[t]["b_end"], c1[t]) == (p["score"], p["b_begin"], p["b_end"], p["cells"])
