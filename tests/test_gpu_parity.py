@@ -234,3 +234,43 @@ def test_reverse_complement_pool_workload(xd):
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=17, X=15)
     ref, rcells = oracle_of(w)
     assert_same(res, cells, ref, rcells, "rc pool")
+
+
+def test_maximum_sizes_and_extreme_scoring(xd):
+    """Reads at XDROP_MAX_READ_LEN (2^18), seed near both ends and the middle, k = 1024, and the
+    largest scores the key range admits (M = 32 over 2^18 bases)."""
+    from synth import workload as W
+    rng = np.random.default_rng(5)
+    L = 1 << 18
+    a = rng.integers(0, 4, size=L, dtype=np.uint8)
+    b = a.copy()
+    mut = rng.random(L) < 0.02
+    b[mut] = (b[mut] + 1) % 4
+    seq = W.ASCII[np.concatenate([a, b])]
+    off = np.array([0, L, 2 * L], np.int64)
+    pairs = np.array([[0, 1, 0, 0], [0, 1, L - 1024, L - 1024], [0, 1, L // 2, L // 2],
+                      [1, 0, 12345, 12345], [0, 0, L // 3, L // 3]], np.int32)   # last: identical read,
+    # score M * 2^18 = 8.4M at M = 32 -- the top of the key range
+    with xd.Aligner() as al:
+        for (k, M, mu, g, X) in [(1024, 1, -1, -1, 15), (17, 32, -64, -64, 40), (31, 2, -3, -2, 0)]:
+            p = pairs.copy()
+            p[:, 2:] = np.minimum(p[:, 2:], L - k)
+            if k == 1024:
+                seq2 = seq.copy()                     # exact 1024-mer seeds
+                for aa, bb, pa, pb in p:
+                    seq2[off[bb] + pb: off[bb] + pb + k] = seq2[off[aa] + pa: off[aa] + pa + k]
+            else:
+                seq2 = seq
+            res, cells = al.align(seq2, off, p, k=k, X=X, M=M, mu=mu, g=g)
+            w2 = W.Workload("max", seq2, off, p, k, X, M, mu, g)
+            ref, rcells = oracle_of(w2)
+            assert_same(res, cells, ref, rcells, f"max k={k} M={M}")
+
+
+def test_length_limit_error(xd):
+    seq = np.frombuffer(b"A" * ((1 << 18) + 1), np.uint8)
+    off = np.array([0, (1 << 18) + 1], np.int64)
+    with xd.Aligner() as al:
+        with pytest.raises(xd.XdropError) as e:
+            al.align(seq, off, np.array([[0, 0, 0, 0]], np.int32), k=5, X=5)
+        assert e.value.status == -6
