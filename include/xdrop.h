@@ -149,6 +149,7 @@ typedef struct {
   int64_t level_cells[4]; /* DP cells of the extensions completed at each level */
   int64_t level_items[4]; /* extensions completed at each level */
   int64_t long_items;     /* extensions run in the multi-lane "long" mode of level 0 */
+  int64_t stolen;         /* lane-mode extensions checkpointed at the tail and resumed 4 lanes wide */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 
@@ -180,6 +181,12 @@ int64_t xdrop_last_trace(const xdrop_ctx* ctx, xdrop_trace_event* buf, int64_t c
 int64_t xdrop_sched_simulate(int m, int policy, int n_ranks, int batch_size, int subbatches,
                              const int64_t* w, int64_t n, double ns_per_unit, xdrop_sched_stats* st,
                              xdrop_trace_event* trace, int64_t cap, int32_t* gpu_of_pair);
+
+/* Work-unit timeline of the last call's band kernel (only when the environment variable
+ * XDROP_TIMELINE is set at xdrop_init): records of 3 x uint64 {type | warp << 8, start_ns,
+ * end_ns}; type 0 lane batch, 1 long batch, 2 stolen batch, 3 lane-pair tier, 4 warp tier.
+ * Returns the number of records (<= cap copied). */
+int64_t xdrop_last_timeline(const xdrop_ctx* ctx, uint64_t* buf, int64_t cap);
 
 /* Alg. 1 ring search over ranks 0..n-1: first rank r,
  * walking down (left) / up (right) from `rank` with wrap-around, with

@@ -110,7 +110,7 @@ class Aligner:
         return dict(items=s.items, escalated=list(s.escalated), kernel_ms=s.kernel_ms, total_ms=s.total_ms,
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
                     level_cells=list(s.level_cells), level_items=list(s.level_items),
-                    long_items=s.long_items)
+                    long_items=s.long_items, stolen=s.stolen)
 
     def sched_stats(self) -> dict:
         s = N.SchedStats()
@@ -124,6 +124,19 @@ class Aligner:
         if n > 0:
             N.lib.xdrop_last_trace(self._h, buf.ctypes.data, n)
         return buf
+
+    def timeline(self) -> np.ndarray:
+        """Work units of the last call's band kernel (XDROP_TIMELINE=1 at construction):
+        rows (type, warp, start_ns, end_ns)."""
+        n = N.lib.xdrop_last_timeline(self._h, None, 0)
+        buf = np.zeros((max(n, 0), 3), dtype=np.uint64)
+        if n > 0:
+            N.lib.xdrop_last_timeline(self._h, buf.ctypes.data, n)
+        out = np.zeros((buf.shape[0], 4), dtype=np.int64)
+        out[:, 0] = (buf[:, 0] & 0xFF).astype(np.int64)
+        out[:, 1] = (buf[:, 0] >> 8).astype(np.int64)
+        out[:, 2:] = buf[:, 1:].astype(np.int64)
+        return out
 
     def int32_peak(self):
         out = np.zeros(2, dtype=np.float64)

@@ -43,7 +43,7 @@ class Stats(ctypes.Structure):
                 ("kernel_ms", ctypes.c_float), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
                 ("launches", ctypes.c_int64), ("level_ms", ctypes.c_float * 4),
                 ("level_cells", ctypes.c_int64 * 4), ("level_items", ctypes.c_int64 * 4),
-                ("long_items", ctypes.c_int64)]
+                ("long_items", ctypes.c_int64), ("stolen", ctypes.c_int64)]
 
 
 class TraceEvent(ctypes.Structure):
@@ -65,6 +65,7 @@ EXPORTS = [
     "xdrop_init", "xdrop_align_batch", "xdrop_align_batch_device", "xdrop_last_stats",
     "xdrop_last_sched_stats", "xdrop_last_trace", "xdrop_sched_simulate", "xdrop_ring_left",
     "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_int32_peak",
+    "xdrop_last_timeline",
 ]
 
 
@@ -95,6 +96,8 @@ def _load():
     lib.xdrop_last_error_index.argtypes = [P]
     lib.xdrop_last_error_index.restype = ctypes.c_int64
     lib.xdrop_int32_peak.argtypes = [P, P]
+    lib.xdrop_last_timeline.argtypes = [P, P, ctypes.c_int64]
+    lib.xdrop_last_timeline.restype = ctypes.c_int64
     return lib
 
 

@@ -65,7 +65,11 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_P2, C_Q2T, C_Q2H,                                  // T2
        C_P3, C_Q3T, C_HEAD3,                                // S = 1024 launch
        C_P4, C_Q4T, C_HEAD4,                                // CTA launch (S = 4096)
-       C_GEN, C_HEADG, C_HEADW, C_N };
+       C_GEN, C_HEADG, C_HEADW,
+       C_IDLE, C_SP, C_ST, C_SH, C_DONES,                   // tail stealing
+       C_TLN,                                               // timeline records
+       C_N };
+constexpr int kTimelineCap = 1 << 16;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 32, HS_LVL = 48, HS_BYTES = 512 };
 
@@ -84,9 +88,12 @@ struct DevCtx {
   int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_cta = 1;
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
+  int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
+  bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
+  float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl;
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -115,6 +122,9 @@ int dev_open(DevCtx& D, int dev) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l0, xk::band_kernel<1, 32>, 128, 0));
   if (const char* e = getenv("XDROP_LONG_G")) D.long_g = atoi(e);
   if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
+  if (const char* e = getenv("XDROP_STEAL_MIN")) D.steal_min = atoi(e);
+  D.timeline = getenv("XDROP_TIMELINE") != nullptr;
+  if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
   if (D.long_g == 2)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
@@ -139,7 +149,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -237,6 +247,10 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     CKR(D.pool3.ensure((size_t)std::max<int64_t>(cap3, 1) * rec3 * sizeof(int)));
     CKR(D.pool4.ensure((size_t)std::max<int64_t>(cap4, 1) * rec4 * sizeof(int)));
     CKR(D.q4.ensure((size_t)std::max<int64_t>(cap4, 1) * sizeof(int)));
+    const int64_t caps = std::min<int64_t>(n_items, 1 << 18);
+    CKR(D.pools.ensure((size_t)std::max<int64_t>(caps, 1) * rec1 * sizeof(int)));
+    CKR(D.qs.ensure((size_t)std::max<int64_t>(caps, 1) * sizeof(int)));
+    CK(cudaMemsetAsync(D.qs.p, 0xff, (size_t)std::max<int64_t>(caps, 1) * sizeof(int), s));
     CKR(D.genl.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
     CK(cudaMemsetAsync(D.ovf1.p, 0xff, (size_t)n_items * sizeof(int), s));
     CK(cudaMemsetAsync(D.ovf2.p, 0xff, (size_t)n_items * sizeof(int), s));
@@ -253,13 +267,24 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       ++launches;
     } else {
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
-                       ctr + C_Q2H};
+                       ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
+                       (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * D.occ_m * 4 * 32), 1 << 30)};
+      if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
+        CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
+        mc.tl = D.tl.as<unsigned long long>(); mc.tl_cap = kTimelineCap;
+      }
+      // tail stealing: when 1/8 of the resident warps are idle, lane warps hand over extensions with
+      // >= 1024 anti-diagonals left (a full block pool falls back to the unbounded kernel)
+      const int nwarps = D.sms * D.occ_m * 4;
+      xk::Esc es{D.pools.as<int>(), rec1, (int)caps, ctr + C_SP, D.qs.as<int>(), ctr + C_ST, gen, ctr + C_GEN};
+      xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
+      if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
       if (D.long_g == 2)
-        xk::band_merged_kernel<32, 2, 16><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
+        xk::band_merged_kernel<32, 2, 16><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (D.long_g == 4)
-        xk::band_merged_kernel<32, 4, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
+        xk::band_merged_kernel<32, 4, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else
-        xk::band_merged_kernel<32, 1, 32><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3);
+        xk::band_merged_kernel<32, 1, 32><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
@@ -290,6 +315,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.escalated[2] = hs[C_P3];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
+    D.st.stolen = hs[C_SP];
     if (n_gen > 0) {
       const int64_t stride = XDROP_MAX_READ_LEN + 8;
       const int warps_per_block = 4;
@@ -630,6 +656,18 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   // stats: sum over devices of the last pipeline runs (per-call granularity for 1 device)
   ctx->st = ctx->devs[0].st;
   return 0;
+}
+
+extern "C" int64_t xdrop_last_timeline(const xdrop_ctx* ctx, uint64_t* buf, int64_t cap) {
+  if (!ctx) return XDROP_EINVAL;
+  const DevCtx& D = ctx->devs[0];
+  if (!D.timeline || !D.tl.p) return 0;
+  int n = 0;
+  if (cudaMemcpy(&n, D.counters.as<int>() + C_TLN, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return XDROP_ECUDA;
+  n = std::min(n, kTimelineCap);
+  if (buf && cap > 0)
+    if (cudaMemcpy(buf, D.tl.p, (size_t)std::min<int64_t>(n, cap) * 24, cudaMemcpyDeviceToHost) != cudaSuccess) return XDROP_ECUDA;
+  return n;
 }
 
 extern "C" int xdrop_last_sched_stats(const xdrop_ctx* ctx, xdrop_sched_stats* st) {

@@ -489,11 +489,30 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
 
 // anti-diagonal loop from each group's own B.d (resumed groups of a warp may sit
 // at different anti-diagonals; all are even at block boundaries)
+// Tail stealing: once `thresh` warps sit idle, a lane-mode warp checkpoints every extension
+// that still has >= min_rem anti-diagonals to go, so idle warps resume it with 4 lanes.
+struct Steal { const int* idle; int thresh; int min_rem; Esc es; };
+
 template <int G, int C>
 __device__ __forceinline__ void band_loop(Band<C>& B, int gl, int& d, int& rem, const Problem& P, int level,
-                                          const Esc& esc) {
+                                          const Esc& esc, const Steal* st = nullptr) {
   constexpr int S = G * C;
+  int blk = 0;
   while (__any_sync(FULL, B.active)) {
+    if (st != nullptr && ((++blk & 31) == 0)) {
+      int go = 0;
+      if ((threadIdx.x & 31) == 0) go = ld_volatile(st->idle) >= st->thresh;
+      go = __shfl_sync(FULL, go, 0);
+      if (go && B.active) {
+        const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
+        const int left = 2 * min(B.m - ic, B.n - (d - ic));   // anti-diagonals still ahead (estimate)
+        if (left >= st->min_rem) {
+          band_save<G, C>(B, gl, d, st->es);
+          B.active = false;
+        }
+      }
+      if (!__any_sync(FULL, B.active)) break;
+    }
     // boundary (i > m or j > n) enters the window?  checked for the later step
     const int d2 = d + 2;
     const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
@@ -517,7 +536,8 @@ __device__ __forceinline__ void band_idle(Band<C>& B) {
 
 // Run one extension from its seed per group of G lanes (item < 0: idle group).  Warp-collective.
 template <int G, int C>
-__device__ __forceinline__ void band_run(const Problem& P, int item, int level, const Esc& esc) {
+__device__ __forceinline__ void band_run(const Problem& P, int item, int level, const Esc& esc,
+                                         const Steal* st = nullptr) {
   constexpr int S = G * C;
   const int gl = (threadIdx.x & 31) % G;
   Band<C> B;
@@ -549,7 +569,7 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
     B.active = false;
   }
   int d = 0;
-  band_loop<G, C>(B, gl, d, rem, P, level, esc);
+  band_loop<G, C>(B, gl, d, rem, P, level, esc, st);
 }
 
 // Resume one checkpointed extension per group (rec == nullptr: idle group) in a
@@ -627,7 +647,24 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 }
 
 // Counters of the merged kernel (ints): see xdrop_capi.cu
-struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head; };
+struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head;
+                   int* idle; int* qs_head; int* dones;
+                   unsigned long long* tl; int* tl_n; int tl_cap;     // optional work-unit timeline
+                   int endgame; };                                    // T0 items left -> 4-lane dispatch
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// timeline record: [type | warp << 8, start_ns, end_ns]
+__device__ __forceinline__ void tl_rec(const MergedCtr& c, int type, unsigned long long t0) {
+  if (c.tl == nullptr || (threadIdx.x & 31) != 0) return;
+  const int i = atomicAdd(c.tl_n, 1);
+  if (i >= c.tl_cap) return;
+  const unsigned long long w = (blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5);
+  c.tl[3 * i] = (unsigned long long)type | (w << 8); c.tl[3 * i + 1] = t0; c.tl[3 * i + 2] = gtimer();
+}
 
 // claim up to `want` published entries of a queue (lane 0 only); returns the
 // first claimed index and sets k (0: nothing claimed)
@@ -668,11 +705,13 @@ __device__ __forceinline__ int wait_entry(const int* q, int i) {
 template <int C0, int GL, int CL>
 __global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
 band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
-                   Esc e1, Esc e2, Esc e3) {
+                   Esc e1, Esc e2, Esc e3, Steal st) {
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
   const int first = (GL > 1) ? n_long : 0;
+  bool idle = false;                    // this warp is counted in *c.idle
+  auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; };
   for (;;) {
     // T2: one checkpointed extension per warp
     {
@@ -684,26 +723,54 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         int slot = 0;
         if (lane == 0) slot = wait_entry(e2.q, h);
         slot = __shfl_sync(FULL, slot, 0);
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
         band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        tl_rec(c, 4, t0);
         continue;
       }
     }
-    // T1: 16 checkpointed extensions per warp (partial batches once T0 is drained)
+    // T1: up to 4 checkpointed extensions per warp, eight lanes x 8 cells each (S = 64),
+    // claimed as soon as they appear: few extensions get here and each one escalated late in
+    // its life, so a short per-anti-diagonal latency matters more than full lanes
     {
-      const bool t0_drained = ld_volatile(c.head_long) >= n_long && first + ld_volatile(c.head0) >= n_items;
       int k = 0, h = 0;
-      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 16, t0_drained, k);
+      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 4, true, k);
       k = __shfl_sync(FULL, k, 0);
       if (k) {
         h = __shfl_sync(FULL, h, 0);
-        const int g = lane >> 1;
+        const int g = lane >> 3;
         int slot = -1;
-        if (g < k && (lane & 1) == 0) slot = wait_entry(e1.q, h + g);
-        slot = __shfl_sync(FULL, slot, lane & ~1);
-        band_resume<2, 32>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        if (g < k && (lane & 7) == 0) slot = wait_entry(e1.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~7);
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        tl_rec(c, 3, t0);
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(c.done1, k);
+        continue;
+      }
+    }
+    // stolen lane-mode extensions: 8 per warp, 4 lanes each (same 32-cell window)
+    {
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.qs_head, st.es.q_tail, 8, true, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        const int g = lane >> 2;
+        int slot = -1;
+        if (g < k && (lane & 3) == 0) slot = wait_entry(st.es.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~3);
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        band_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        tl_rec(c, 2, t0);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.dones, k);
         continue;
       }
     }
@@ -714,34 +781,59 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       base = __shfl_sync(FULL, base, 0);
       if (base < n_long) {
         const int slot = base + lane / GL;
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
         band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        tl_rec(c, 1, t0);
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(c.done0, min(32 / GL, n_long - base));
         continue;
       }
     }
-    // T0: the rest, 32 per warp (lane per extension)
-    int base = n_items;
-    if (lane == 0 && first + ld_volatile(c.head0) < n_items) base = first + atomicAdd(c.head0, 32);
+    // T0: the rest, 32 per warp (lane per extension); in the endgame (less than `endgame`
+    // extensions left in the queue) 8 per warp with 4 lanes each, to shorten the tail
+    int base = n_items, take = 32;
+    if (lane == 0) {
+      const int h0 = first + ld_volatile(c.head0);
+      if (h0 < n_items) {
+        take = (n_items - h0 < c.endgame) ? 8 : 32;
+        base = first + atomicAdd(c.head0, take);
+      }
+    }
     base = __shfl_sync(FULL, base, 0);
+    take = __shfl_sync(FULL, take, 0);
     if (base < n_items) {
-      const int slot = base + lane;
-      band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1);
+      busy();
+      const unsigned long long t0 = c.tl ? gtimer() : 0;
+      if (take == 32) {
+        const int slot = base + lane;
+        band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+        tl_rec(c, 0, t0);
+      } else {
+        const int slot = base + (lane >> 2);
+        band_run<4, 8>(P, slot < min(base + 8, n_items) ? items[slot] : -1, 0, e1);
+        tl_rec(c, 5, t0);
+      }
       __threadfence();
       __syncwarp();
-      if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
+      if (lane == 0) atomicAdd(c.done0, min(take, n_items - base));
       continue;
     }
     // no work visible: finished once T0 is done (=> T1's queue is final), T1 is
     // done (=> T2's queue is final) and T2's queue is drained
+    // (stolen records come only from T0 batches, before their done0 add)
     int fin = 0;
     if (lane == 0) {
       if (ld_volatile(c.done0) >= n_items) {
-        const int t1 = ld_volatile(e1.q_tail);
-        if (ld_volatile(c.done1) >= t1 && ld_volatile(c.q1_head) >= t1)
-          fin = ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
+        const int ts = ld_volatile(st.es.q_tail);
+        if (ld_volatile(c.dones) >= ts && ld_volatile(c.qs_head) >= ts) {
+          const int t1 = ld_volatile(e1.q_tail);
+          if (ld_volatile(c.done1) >= t1 && ld_volatile(c.q1_head) >= t1)
+            fin = ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
+        }
       }
+      if (!fin && !idle) { atomicAdd(c.idle, 1); idle = true; }
     }
     fin = __shfl_sync(FULL, fin, 0);
     if (fin) break;

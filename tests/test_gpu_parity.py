@@ -274,3 +274,30 @@ def test_length_limit_error(xd):
         with pytest.raises(xd.XdropError) as e:
             al.align(seq, off, np.array([[0, 0, 0, 0]], np.int32), k=5, X=5)
         assert e.value.status == -6
+
+
+@pytest.mark.parametrize("steal_min", ["0", "16", "200"])
+def test_tail_stealing_resumes_exactly(xd, steal_min, monkeypatch):
+    """Lane-mode extensions checkpointed at the tail and resumed 4 lanes wide stay exact."""
+    from synth import workload as W
+    monkeypatch.setenv("XDROP_STEAL_MIN", steal_min)
+    monkeypatch.setenv("XDROP_LONG_G", "0")           # keep every extension in lane mode first
+    w = W.random_pairs_workload(seed=77, n_pairs=300, len_lo=500, len_hi=4000, k=15, X=15, rc_frac=0.3)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, f"steal {steal_min}")
+    if steal_min == "16":
+        assert st["stolen"] > 0
+
+
+def test_endgame_dispatch_exact(xd, monkeypatch):
+    """The optional 4-lane endgame dispatch of T0 (XDROP_ENDGAME) stays exact."""
+    from synth import workload as W
+    monkeypatch.setenv("XDROP_ENDGAME", "100")        # every T0 batch in endgame mode
+    w = W.random_pairs_workload(seed=78, n_pairs=200, len_lo=0, len_hi=2000, k=15, X=20, rc_frac=0.3)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, "endgame")
