@@ -90,6 +90,7 @@ struct DevCtx {
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
+  bool pk16 = true;          // packed 16-bit lane mode for T0 (XDROP_PK16=0: 32-bit lane mode)
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
@@ -125,13 +126,19 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_STEAL_MIN")) D.steal_min = atoi(e);
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
+  if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
   if (D.long_g == 2)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16, false>, 128, 0));
   else if (D.long_g == 4)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8, false>, 128, 0));
+  if (D.long_g == 4) {
+    int o = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, xk::band_merged_kernel<32, 4, 8, true>, 128, 0));
+    D.occ_m = std::min(D.occ_m, std::max(1, o));
+  }
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32, false>, 128, 0));
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_resume_kernel<32, 32>, 128, 0));
@@ -218,6 +225,9 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   P.pairs = pairs; P.n_pairs = n_pairs;
   P.M = p.match; P.mu = p.mismatch; P.g = p.gap; P.X = p.xdrop; P.k = p.k;
   P.keym = 1 << xk::KEYSH;
+  P.pkM = 32 * (p.match - 2 * p.gap); P.pkU = 32 * (p.mismatch - 2 * p.gap);
+  // packed 16-bit lane mode (xdrop_pk16.cuh) whenever its value range holds
+  const bool pk = D.pk16 && p.xdrop + p.match <= 510;
   P.ext = D.ext.as<ExtOut>();
 
   int* ctr = D.counters.as<int>();
@@ -280,11 +290,13 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
       if (D.long_g == 2)
-        xk::band_merged_kernel<32, 2, 16><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 2, 16, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (D.long_g == 4 && pk)
+        xk::band_merged_kernel<32, 4, 8, true><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (D.long_g == 4)
-        xk::band_merged_kernel<32, 4, 8><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 4, 8, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else
-        xk::band_merged_kernel<32, 1, 32><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 1, 32, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));

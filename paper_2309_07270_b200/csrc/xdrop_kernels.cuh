@@ -52,6 +52,7 @@ struct Problem {
   const PairDesc* pairs; int64_t n_pairs;
   int M, mu, g, X, k;
   int keym;          // 128: argmax key multiplier, passed at run time so ptxas keeps it an IMAD (FMA pipe)
+  int pkM, pkU;      // packed lane mode: 32 * (M - 2g), 32 * (mu - 2g)
   ExtOut* ext;
 };
 
@@ -646,6 +647,8 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   }
 }
 
+#include "xdrop_pk16.cuh"
+
 // Counters of the merged kernel (ints): see xdrop_capi.cu
 struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head;
                    int* idle; int* qs_head; int* dones;
@@ -702,7 +705,7 @@ __device__ __forceinline__ int wait_entry(const int* q, int i) {
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
-template <int C0, int GL, int CL>
+template <int C0, int GL, int CL, bool PK>
 __global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
 band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                    Esc e1, Esc e2, Esc e3, Steal st) {
@@ -808,7 +811,8 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       const unsigned long long t0 = c.tl ? gtimer() : 0;
       if (take == 32) {
         const int slot = base + lane;
-        band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+        if constexpr (PK) pk_run(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+        else band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
         tl_rec(c, 0, t0);
       } else {
         const int slot = base + (lane >> 2);
