@@ -705,8 +705,14 @@ __device__ __forceinline__ int wait_entry(const int* q, int i) {
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
+#ifndef XDROP_PK_C
+#define XDROP_PK_C 32          // cells per lane of the packed lane mode
+#endif
+#ifndef XDROP_PK_MINBLOCKS
+#define XDROP_PK_MINBLOCKS 4
+#endif
 template <int C0, int GL, int CL, bool PK>
-__global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
+__global__ void __launch_bounds__(128, PK ? XDROP_PK_MINBLOCKS : XDROP_MERGED_MINBLOCKS)
 band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                    Esc e1, Esc e2, Esc e3, Steal st) {
   const int lane = threadIdx.x & 31;
@@ -786,7 +792,8 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         const int slot = base + lane / GL;
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        if constexpr (PK) pk_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        else band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
         tl_rec(c, 1, t0);
         __threadfence();
         __syncwarp();
@@ -811,7 +818,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       const unsigned long long t0 = c.tl ? gtimer() : 0;
       if (take == 32) {
         const int slot = base + lane;
-        if constexpr (PK) pk_run(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+        if constexpr (PK) pk_run<1, XDROP_PK_C>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
         else band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
         tl_rec(c, 0, t0);
       } else {

@@ -1,16 +1,19 @@
-// xdrop_pk16.cuh -- packed 16-bit lane mode of tier T0 (included by xdrop_kernels.cuh).
+// xdrop_pk16.cuh -- packed 16-bit band mode of tier T0 (included by xdrop_kernels.cuh).
 //
-// Same operation as band_run<1, 32> (one extension per lane, a window of 32
-// cells per anti-diagonal = 64 diagonals, re-centred by band shifts, exact
-// checkpoints to the 32-bit tiers), but the cells of an anti-diagonal are held
-// as 16 PAIRS of 16-bit values and updated with the sm_100a dynamic-programming
-// instructions (VIMNMX.S16x2 / VIADDMNMX.S16x2), two cells per instruction.
+// Same operation as band_run<G, 32/G> (G lanes per extension, a window of 32
+// cells per anti-diagonal = 64 diagonals, exact checkpoints to the 32-bit
+// tiers), but the cells of an anti-diagonal are held as PAIRS of 16-bit values
+// and updated with the sm_100a dynamic-programming instructions
+// (VIMNMX.S16x2 / VIADDMNMX.S16x2), two cells per instruction.  G = 1 is the
+// lane-per-extension mode; G = 2 / 4 shorten the anti-diagonal chain of the
+// longest extensions (the launch's critical path).
 //
-// Layout.  Cell t (0..31) of parity p sits on diagonal K0 + 2t + p.  Pair u of
-// a parity array holds cells (u, u + 16) -- lo and hi half.  With this strided
+// Layout.  Cell t (0..31) of parity p sits on diagonal K0 + 2t + p; lane gl of
+// a group owns cells t = gl*C + tl, tl < C = 32/G.  Pair u of a parity array
+// holds local cells (u, u + NP), NP = C/2 -- lo and hi half.  With this strided
 // pairing the two neighbours of every pair are again whole pairs (for even
 // cells: odd pairs u-1 and u; for odd cells: even pairs u and u+1); only the
-// pair at the seam needs one PRMT.
+// pair at the seam needs one PRMT (and one shuffle from the next lane).
 //
 // Values.  A cell of anti-diagonal d is stored RELATIVE to the pruning
 // threshold of d and scaled by 32:  v = 32 * (W - thrW_d) + (31 - t), W the
@@ -35,19 +38,6 @@ namespace pk {
 constexpr uint32_t DEAD2 = 0xC000C000u;    // a pair of dead cells
 constexpr uint32_t KILLC = 0xC01FC01Fu;    // LOP3 constant: bits taken from the PRMT mask
 constexpr uint32_t NOFLOOR = 0x80008000u;  // no-op third operand of VIADDMNMX
-// 31 - t key bytes: TCW(j) = [31-2j, 15-2j, 30-2j, 14-2j] (pairs 2j and 2j+1, lo / hi cell)
-__host__ __device__ constexpr uint32_t TCW(int j) {
-  return (uint32_t)(31 - 2 * j) | ((uint32_t)(15 - 2 * j) << 8) | ((uint32_t)(30 - 2 * j) << 16) |
-         ((uint32_t)(14 - 2 * j) << 24);
-}
-// PRMT mask of pair u with no dead cell: [31-u, 0, 15-u, 0]
-__host__ __device__ constexpr uint32_t MTC(int u) { return (uint32_t)(31 - u) | ((uint32_t)(15 - u) << 16); }
-// chain c (pairs 8c .. 8c+7) accumulates sum_j 2^(7-j) m(8c+j); its key-byte part:
-__host__ __device__ constexpr uint32_t CHC(int c) {
-  uint32_t s = 0;
-  for (int j = 0; j < 8; ++j) s = s * 2u + MTC(8 * c + j);
-  return s;
-}
 constexpr uint32_t INV255 = 0xFEFEFFu;     // 255^-1 mod 2^24
 }  // namespace pk
 
@@ -55,6 +45,18 @@ constexpr uint32_t INV255 = 0xFEFEFFu;     // 255^-1 mod 2^24
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// out = c ? b : (a & ~b) bitwise, as ONE LOP3 (the compiler splits the C form in two)
+__device__ __forceinline__ uint32_t lop_kill(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x98;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// an opaque copy (keeps a loop-invariant constant in a register instead of rematerialising it)
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t d;
+  asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(x));
   return d;
 }
 // bits 0, 2, .., 30 of x -> bits 0..15
@@ -70,9 +72,11 @@ __device__ __forceinline__ uint32_t plane32(uint64_t w, int b) {
   return even_bits16((uint32_t)(w >> b)) | (even_bits16((uint32_t)(w >> 32 >> b)) << 16);
 }
 
-struct Band16 {
-  uint32_t E[16], O[16];          // even / odd cells, pair u = (cell u, cell u + 16)
-  uint32_t A0, A1, B0, B1;        // bit planes: bit t <-> a[ia0 + t], b[jb0 - t] (b complemented for RC)
+template <int G, int C> struct Band16 {
+  static constexpr int NP = C / 2;
+  uint32_t E[NP], O[NP];          // even / odd cells, pair u = (local cell u, local cell u + NP)
+  uint32_t TC[NP / 2];            // key bytes 31 - t of pairs 2j, 2j+1: [lo(2j), hi(2j), lo(2j+1), hi(2j+1)]
+  uint32_t A0, A1, B0, B1;        // bit planes: bit tl <-> a[ia0 + C gl + tl], b[jb0 - C gl - tl] (b ^ cm)
   uint32_t An0, An1, Bn0, Bn1;    // reservoir planes: next a at bit 0 (>>), next b at bit 31 (<<)
   uint32_t Anr, Bnr;              // raw codes of the next reservoir refill (16 bases each)
   uint32_t cm;                    // ~0: b complemented
@@ -81,14 +85,26 @@ struct Band16 {
   int best, istar, jstar, dbase;  // best: H + BIAS
   int thrD1, thrD, thrN;          // W-space thresholds of anti-diagonals d-1, d and d+1
   int minL1, maxL1, minL2, maxL2;
-  long long cells;
+  int cells;                      // < 2^19 anti-diagonals x 32 cells
   int item;
   bool active;
 };
 
+// key bytes 31 - t; `zero` is an opaque 0 so the words stay in registers (PRMT operand c)
+template <int G, int C>
+__device__ __forceinline__ void pk_keys(Band16<G, C>& B, int gl, int zero) {
+  constexpr int NP = C / 2;
+  const int tb = 31 - C * gl + zero;
+#pragma unroll
+  for (int j = 0; j < NP / 2; ++j)
+    B.TC[j] = opaque((uint32_t)(tb - 2 * j) | ((uint32_t)(tb - 2 * j - NP) << 8) |
+                     ((uint32_t)(tb - 2 * j - 1) << 16) | ((uint32_t)(tb - 2 * j - 1 - NP) << 24));
+}
+
 // window + reservoirs at (ia0, jb0); `rem` blocks until the next refill
-__device__ __forceinline__ void pk_reload(Band16& B, int rem, const Problem& P) {
-  const int ia = B.ia0, jb = B.jb0;
+template <int G, int C>
+__device__ __forceinline__ void pk_reload(Band16<G, C>& B, int gl, int rem, const Problem& P) {
+  const int ia = B.ia0 + C * gl, jb = B.jb0 - C * gl;
   const uint64_t aw = load32c(P.PA, B.sa, B.da, ia);
   B.A0 = plane32(aw, 0); B.A1 = plane32(aw, 1);
   const uint64_t ar = load32c(P.PA, B.sa, B.da, ia + 32);
@@ -103,11 +119,31 @@ __device__ __forceinline__ void pk_reload(Band16& B, int rem, const Problem& P) 
   B.Bnr = load16(P.PB, B.sb, B.db, jb + 17 + rem);
 }
 
+// max over k[0..N) of packed 16-bit keys (tree of VIMNMX3.S16x2)
+template <int N>
+__device__ __forceinline__ uint32_t tree16(const uint32_t (&k)[N]) {
+  if constexpr (N == 1) {
+    return k[0];
+  } else {
+    constexpr int M = (N + 2) / 3;
+    uint32_t t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (3 * i + 2 < N) t[i] = __vimax3_s16x2(k[3 * i], k[(3 * i + 1) % N], k[(3 * i + 2) % N]);
+      else if (3 * i + 1 < N) t[i] = __vmaxs2(k[3 * i], k[(3 * i + 1) % N]);
+      else t[i] = k[3 * i];
+    }
+    return tree16<M>(t);
+  }
+}
+
 // One anti-diagonal d of parity PAR: V (parity PAR, holds d-2) is updated in place from
 // N (holds d-1).  CHECK: cells with q outside [qlo, qhi] (beyond the matrix) are dead.
-template <int PAR, bool CHECK>
-__device__ __forceinline__ void pk_cells(uint32_t (&V)[16], const uint32_t (&N)[16], const Band16& B, int qlo,
-                                         int qhi, const Problem& P, uint32_t& kout, uint32_t& ch0, uint32_t& ch1) {
+// Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
+template <int G, int C, int PAR, bool CHECK>
+__device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<G, C>& B,
+                                             int gl, int qlo, int qhi, const Problem& P, uint32_t (&ch)[C > 16 ? 2 : 1]) {
+  constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
   const int thr_d = B.thrN;
   const int D1 = 32 * (B.thrD - thr_d);
   const int Ev = 32 * (B.thrD1 - B.thrD);
@@ -117,18 +153,34 @@ __device__ __forceinline__ void pk_cells(uint32_t (&V)[16], const uint32_t (&N)[
   // of a negative lo half (the hi-half product drops it mod 2^32)
   const uint32_t kk = (uint32_t)(sU - sM) + ((sU < 0 && sM >= 0) ? 0x10000u : 0u);
   const uint32_t D1p = __byte_perm((uint32_t)D1, 0u, 0x1010);
-  const uint32_t mis = (B.A0 ^ B.B0) | (B.A1 ^ B.B1);     // bit t: cell t compares unequal bases
+  uint32_t mis = (B.A0 ^ B.B0) | (B.A1 ^ B.B1);           // bit tl: local cell tl compares unequal bases
+  if constexpr (NP < 16) {                                // hi cells (tl >= NP) to bits 16..
+    constexpr uint32_t LO = (1u << NP) - 1u;
+    mis = (mis & LO) | ((mis << (16 - NP)) & (LO << 16));
+  }
   const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
-  ch0 = 0; ch1 = 0;
+  // seam pair: the neighbour cell beyond the lane's last (first) cell
+  uint32_t seam;
+  if constexpr (PAR == 0) {
+    uint32_t x = pk::DEAD2;
+    if constexpr (G > 1) { x = __shfl_up_sync(FULL, N[NP - 1], 1, G); if (gl == 0) x = pk::DEAD2; }
+    seam = __byte_perm(N[NP - 1], x, 0x1076);            // (left lane's last odd cell, own odd cell NP-1)
+  } else {
+    uint32_t x = pk::DEAD2;
+    if constexpr (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
+    seam = __byte_perm(N[0], x, 0x5432);                 // (own even cell NP, right lane's even cell 0)
+  }
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
+  for (int c = 0; c < NCH; ++c) ch[c] = 0;
+#pragma unroll
+  for (int u = 0; u < NP; ++u) {
     uint32_t L, R;
     if constexpr (PAR == 0) {
-      L = (u == 0) ? __byte_perm(N[15], pk::DEAD2, 0x1054) : N[u == 0 ? 0 : u - 1];
+      L = (u == 0) ? seam : N[u == 0 ? 0 : u - 1];
       R = N[u];
     } else {
       L = N[u];
-      R = (u == 15) ? __byte_perm(N[0], pk::DEAD2, 0x7632) : N[u == 15 ? 0 : u + 1];
+      R = (u == NP - 1) ? seam : N[u == NP - 1 ? 0 : u + 1];
     }
     const uint32_t nb = __vmaxs2(L, R);
     const uint32_t sh = (u == 0) ? mis : __umulhi(mis, 1u << (32 - u));
@@ -136,48 +188,62 @@ __device__ __forceinline__ void pk_cells(uint32_t (&V)[16], const uint32_t (&N)[
     uint32_t v = __viaddmax_s16x2(V[u], sE, nb);
     v = __viaddmax_s16x2(v, D1p, pk::NOFLOOR);
     if constexpr (CHECK) {
-      const int q0 = 2 * u + PAR, q1 = q0 + 32;
+      const int q0 = 2 * (C * gl + u) + PAR, q1 = q0 + 2 * NP;
       const uint32_t cap = ((q0 >= qlo && q0 <= qhi) ? 0x7FFFu : 0x8000u) |
                            ((q1 >= qlo && q1 <= qhi) ? 0x7FFF0000u : 0x80000000u);
       v = __vmins2(v, cap);
     }
     // [31-t(lo), sign(lo) x 8, 31-t(hi), sign(hi) x 8]
-    const uint32_t tcw = (u >> 1) == 0 ? pk::TCW(0) : (u >> 1) == 1 ? pk::TCW(1) : (u >> 1) == 2 ? pk::TCW(2)
-                       : (u >> 1) == 3 ? pk::TCW(3) : (u >> 1) == 4 ? pk::TCW(4) : (u >> 1) == 5 ? pk::TCW(5)
-                       : (u >> 1) == 6 ? pk::TCW(6) : pk::TCW(7);
-    const uint32_t m = prmt(v, tcw, (u & 1) ? 0xB796u : 0xB594u);
-    v = (pk::KILLC & m) | (~pk::KILLC & v & ~m);
+    const uint32_t m = prmt(v, B.TC[u >> 1], (u & 1) ? 0xB796u : 0xB594u);
+    v = lop_kill(v, m, pk::KILLC);
     V[u] = v;
-    if (u < 8) ch0 = ch0 * two + m;
-    else ch1 = ch1 * two + m;
+    ch[u / NPC] = ch[u / NPC] * two + m;
   }
-  // argmax key tree (lo cells carry larger keys than hi cells of equal value: smaller t wins)
-  uint32_t k5[6];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) k5[i] = __vimax3_s16x2(V[3 * i], V[3 * i + 1], V[3 * i + 2]);
-  k5[5] = V[15];
-  kout = __vmaxs2(__vimax3_s16x2(k5[0], k5[1], k5[2]), __vimax3_s16x2(k5[3], k5[4], k5[5]));
+  return tree16<NP>(V);
 }
 
-template <int PAR, bool CHECK>
-__device__ __forceinline__ void pk_diag(Band16& B, int d, int qlo, int qhi, const Problem& P) {
-  uint32_t kk, ch0, ch1;
-  if constexpr (PAR == 0) pk_cells<0, CHECK>(B.E, B.O, B, qlo, qhi, P, kk, ch0, ch1);
-  else pk_cells<1, CHECK>(B.O, B.E, B, qlo, qhi, P, kk, ch0, ch1);
+// dead bits of the lane (local cell tl at bit C-1-tl) from the mask chains
+template <int C>
+__device__ __forceinline__ uint32_t pk_dead(const uint32_t (&ch)[C > 16 ? 2 : 1], const uint32_t (&chc)[C > 16 ? 2 : 1]) {
+  constexpr int NP = C / 2, NPC = C > 16 ? NP / 2 : NP;
+  if constexpr (C == 32) {
+    const uint32_t y0 = ((ch[0] - chc[0]) >> 8) * pk::INV255;   // [A8, 0, B8, -]: cells 0-7, 16-23
+    const uint32_t y1 = ((ch[1] - chc[1]) >> 8) * pk::INV255;   //                 cells 8-15, 24-31
+    return __byte_perm(y0, y1, 0x0426);
+  } else if constexpr (C > 16) {
+    const uint32_t y0 = ((ch[0] - chc[0]) >> 8) * pk::INV255;
+    const uint32_t y1 = ((ch[1] - chc[1]) >> 8) * pk::INV255;
+    return ((y0 & 0xffu) << (C - NPC)) | ((y1 & 0xffu) << (C - 2 * NPC)) | (((y0 >> 16) & 0xffu) << NPC) |
+           ((y1 >> 16) & 0xffu);
+  } else {
+    const uint32_t y = ((ch[0] - chc[0]) >> 8) * pk::INV255;    // [A, 0, B, -]: A bit NP-1-u: cell u
+    return ((y & 0xffu) << NP) | ((y >> 16) & 0xffu);
+  }
+}
+
+template <int G, int C, int PAR, bool CHECK>
+__device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo, int qhi, const Problem& P,
+                                        const uint32_t (&chc)[C > 16 ? 2 : 1]) {
+  uint32_t ch[C > 16 ? 2 : 1];
+  uint32_t kk;
+  if constexpr (PAR == 0) kk = pk_cells<G, C, 0, CHECK>(B.E, B.O, B, gl, qlo, qhi, P, ch);
+  else kk = pk_cells<G, C, 1, CHECK>(B.O, B.E, B, gl, qlo, qhi, P, ch);
   const int thr_d = B.thrN;
-  const int kmax = max((int)(int16_t)(kk & 0xffffu), ((int)kk) >> 16);
+  const int kmax = gmax<G>(max((int)(int16_t)(kk & 0xffffu), ((int)kk) >> 16));
   const bool live = kmax >= 0;
   const int vrel = kmax >> 5;
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
   B.thrN = thr_d + (live ? max(0, vrel - P.X) : 0) - P.g;
-  // ---- dead bits (cell t at bit 31 - t) from the two mask chains
-  const uint32_t y0 = ((ch0 - pk::CHC(0)) >> 8) * pk::INV255;   // [A8, 0, B8, -]: cells 0-7, 16-23
-  const uint32_t y1 = ((ch1 - pk::CHC(1)) >> 8) * pk::INV255;   //                 cells 8-15, 24-31
-  const uint32_t dbits = __byte_perm(y0, y1, 0x0426);
-  const unsigned lb = ~dbits;
-  const int tmin = lb ? (int)__clz(lb) : EMIN;
-  const int tmax = lb ? 32 - __ffs(lb) : EMAX;
+  // ---- off the critical path: live extent, best / argmax, hull count
+  const uint32_t dl = pk_dead<C>(ch, chc);
+  const unsigned lb = ~dl & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  int tmin = (__clz(lb) - (32 - C)) + C * gl;
+  int tmax = (C - __ffs(lb)) + C * gl;
+  tmin = lb ? tmin : EMIN;
+  tmax = lb ? tmax : EMAX;
+  tmin = gmin<G>(tmin);
+  tmax = gmax<G>(tmax);
   const int ibase = (d + B.K0 + PAR) >> 1;
   const int woff = -P.g * (d - B.dbase);
   const int gv = thr_d + vrel - woff;
@@ -188,7 +254,7 @@ __device__ __forceinline__ void pk_diag(Band16& B, int d, int qlo, int qhi, cons
   B.jstar = up ? d - ibase - tst : B.jstar;
   const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
   const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
-  B.cells += (B.active && hi >= lo) ? (long long)(hi - lo + 1) : 0ll;
+  B.cells += (B.active && hi >= lo) ? hi - lo + 1 : 0;
   B.minL2 = B.minL1; B.maxL2 = B.maxL1;
   B.minL1 = (tmin == EMIN) ? EMIN : ibase + tmin;
   B.maxL1 = (tmax == EMAX) ? EMAX : ibase + tmax;
@@ -203,56 +269,86 @@ __device__ __forceinline__ void pk_diag(Band16& B, int d, int qlo, int qhi, cons
   }
 }
 
-// shift the window by 2K diagonals: cell t <- cell t + K (both parities)
-template <int K>
-__device__ __forceinline__ void pk_shift_arr(uint32_t (&A)[16]) {
-  uint32_t T[16];
+// lane mode: shift the window by 2K diagonals: cell t <- cell t + K (both parities)
+template <int NP, int K>
+__device__ __forceinline__ void pk_shift_arr(uint32_t (&A)[NP]) {
+  uint32_t T[NP];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
+  for (int u = 0; u < NP; ++u) {
     if constexpr (K > 0) {
-      if (u + K < 16) T[u] = A[(u + K) & 15];
-      else T[u] = __byte_perm(A[(u + K - 16) & 15], pk::DEAD2, 0x7632);   // (old hi, dead)
+      if (u + K < NP) T[u] = A[(u + K) % NP];
+      else T[u] = __byte_perm(A[(u + K - NP + NP) % NP], pk::DEAD2, 0x7632);   // (old hi, dead)
     } else {
-      if (u + K >= 0) T[u] = A[(u + K + 16) & 15];
-      else T[u] = __byte_perm(A[(u + K + 16) & 15], pk::DEAD2, 0x1054);   // (dead, old lo)
+      if (u + K >= 0) T[u] = A[(u + K + NP) % NP];
+      else T[u] = __byte_perm(A[(u + K + NP) % NP], pk::DEAD2, 0x1054);        // (dead, old lo)
     }
   }
 #pragma unroll
-  for (int u = 0; u < 16; ++u) A[u] = T[u];
+  for (int u = 0; u < NP; ++u) A[u] = T[u];
 }
-template <int K>
-__device__ __forceinline__ void pk_shift_k(Band16& B) { pk_shift_arr<K>(B.E); pk_shift_arr<K>(B.O); }
-__device__ __forceinline__ void pk_shift_n(Band16& B, int s) {
+template <int C, int K>
+__device__ __forceinline__ void pk_shift_k(Band16<1, C>& B) {
+  pk_shift_arr<C / 2, K>(B.E); pk_shift_arr<C / 2, K>(B.O);
+}
+template <int C>
+__device__ __forceinline__ void pk_shift_n(Band16<1, C>& B, int s) {
   switch (s) {
-    case 1: pk_shift_k<1>(B); break;   case -1: pk_shift_k<-1>(B); break;
-    case 2: pk_shift_k<2>(B); break;   case -2: pk_shift_k<-2>(B); break;
-    case 3: pk_shift_k<3>(B); break;   case -3: pk_shift_k<-3>(B); break;
-    case 4: pk_shift_k<4>(B); break;   case -4: pk_shift_k<-4>(B); break;
-    case 5: pk_shift_k<5>(B); break;   case -5: pk_shift_k<-5>(B); break;
-    case 6: pk_shift_k<6>(B); break;   case -6: pk_shift_k<-6>(B); break;
-    case 7: pk_shift_k<7>(B); break;   case -7: pk_shift_k<-7>(B); break;
-    case 8: pk_shift_k<8>(B); break;   case -8: pk_shift_k<-8>(B); break;
+    case 1: pk_shift_k<C, 1>(B); break;   case -1: pk_shift_k<C, -1>(B); break;
+    case 2: pk_shift_k<C, 2>(B); break;   case -2: pk_shift_k<C, -2>(B); break;
+    case 3: pk_shift_k<C, 3>(B); break;   case -3: pk_shift_k<C, -3>(B); break;
+    case 4: pk_shift_k<C, 4>(B); break;   case -4: pk_shift_k<C, -4>(B); break;
+    case 5: pk_shift_k<C, 5>(B); break;   case -5: pk_shift_k<C, -5>(B); break;
+    case 6: pk_shift_k<C, 6>(B); break;   case -6: pk_shift_k<C, -6>(B); break;
+    case 7: pk_shift_k<C, 7>(B); break;   case -7: pk_shift_k<C, -7>(B); break;
+    case 8: pk_shift_k<C, 8>(B); break;   case -8: pk_shift_k<C, -8>(B); break;
     default: break;
   }
 }
+// group mode: shift by one cell (dir = +1: cell t <- t + 1), across the group's lanes
+template <int G, int NP>
+__device__ __forceinline__ void pk_shift1(uint32_t (&A)[NP], int gl, int dir) {
+  const unsigned gm = group_mask<G>();
+  if (dir > 0) {
+    uint32_t x = __shfl_down_sync(gm, A[0], 1, G);
+    if (gl == G - 1) x = pk::DEAD2;
+    const uint32_t last = __byte_perm(A[0], x, 0x5432);
+#pragma unroll
+    for (int u = 0; u < NP - 1; ++u) A[u] = A[u + 1];
+    A[NP - 1] = last;
+  } else {
+    uint32_t x = __shfl_up_sync(gm, A[NP - 1], 1, G);
+    if (gl == 0) x = pk::DEAD2;
+    const uint32_t first = __byte_perm(A[NP - 1], x, 0x1076);
+#pragma unroll
+    for (int u = NP - 1; u >= 1; --u) A[u] = A[u - 1];
+    A[0] = first;
+  }
+}
 
-// checkpoint in the 32-bit record format of band_save (S = 32; d even: E holds d, O holds d-1)
-__device__ __forceinline__ void pk_save(const Band16& B, int d, const Esc& e) {
-  const int slot = atomicAdd(e.pool_tail, 1);
+// checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
+template <int G, int C>
+__device__ __forceinline__ void pk_save(const Band16<G, C>& B, int gl, int d, const Esc& e) {
+  constexpr int NP = C / 2;
+  const unsigned gm = group_mask<G>();
+  int slot = 0;
+  if (gl == 0) slot = atomicAdd(e.pool_tail, 1);
+  if constexpr (G > 1) slot = __shfl_sync(gm, slot, 0, G);
   if (slot >= e.cap) {
-    push_item(e.fb_items, e.fb_tail, B.item);
+    if (gl == 0) push_item(e.fb_items, e.fb_tail, B.item);
     return;
   }
   int* rec = e.pool + (size_t)slot * e.rec_ints;
-  rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrN; rec[5] = B.best;
-  rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
-  rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = 32;
-  rec[15] = (int)(B.cells & 0xffffffffll); rec[16] = (int)(B.cells >> 32);
+  if (gl == 0) {
+    rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrN; rec[5] = B.best;
+    rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
+    rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = G * C;
+    rec[15] = B.cells; rec[16] = 0;
+  }
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
+  for (int u = 0; u < NP; ++u) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int t = u + 16 * h;
+      const int t = C * gl + u + NP * h;
       const int ve = h ? ((int)B.E[u] >> 16) : (int)(int16_t)(B.E[u] & 0xffffu);
       const int vo = h ? ((int)B.O[u] >> 16) : (int)(int16_t)(B.O[u] & 0xffffu);
       rec[HDR + 2 * t] = ve >= 0 ? B.thrD + (ve >> 5) : NEGV;
@@ -260,13 +356,15 @@ __device__ __forceinline__ void pk_save(const Band16& B, int d, const Esc& e) {
     }
   }
   __threadfence();
-  push_item(e.q, e.q_tail, slot);
+  if constexpr (G > 1) __syncwarp(gm);
+  if (gl == 0) push_item(e.q, e.q_tail, slot);
 }
 
-// end of a block of two anti-diagonals (as band_block_end<1, 32>)
-__device__ __forceinline__ void pk_block_end(Band16& B, int d, int& rem, const Problem& P, int level,
+// end of a block of two anti-diagonals (as band_block_end<G, C>)
+template <int G, int C>
+__device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int& rem, const Problem& P, int level,
                                              const Esc& esc) {
-  constexpr int S = 32;
+  constexpr int S = G * C;
   if (d - B.dbase >= 1024) {      // keep W bounded for the 32-bit tiers' checkpoints
     const int woff = -P.g * (d - B.dbase);
     B.thrD1 -= woff; B.thrD -= woff; B.thrN -= woff;
@@ -278,45 +376,67 @@ __device__ __forceinline__ void pk_block_end(Band16& B, int d, int& rem, const P
       B.An0 |= even_bits16(B.Anr) << 16; B.An1 |= even_bits16(B.Anr >> 1) << 16;
       B.Bn0 |= ((__brev(even_bits16(B.Bnr)) ^ B.cm) >> 16);
       B.Bn1 |= ((__brev(even_bits16(B.Bnr >> 1)) ^ B.cm) >> 16);
-      B.Anr = load16(P.PA, B.sa, B.da, B.ia0 + 64);
-      B.Bnr = load16(P.PB, B.sb, B.db, B.jb0 + 33);
+      B.Anr = load16(P.PA, B.sa, B.da, B.ia0 + C * gl + 64);
+      B.Bnr = load16(P.PB, B.sb, B.db, B.jb0 - C * gl + 33);
     }
   }
   if (!B.active) return;
   const bool e0 = (B.minL1 == EMIN), e1 = (B.minL2 == EMIN);
   if ((e0 && e1) || d >= B.m + B.n) {
-    ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
-    o.cells = B.cells; o.pad = 0;
-    P.ext[B.item] = o;
+    if (gl == 0) {
+      ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
+      o.cells = B.cells; o.pad = 0;
+      P.ext[B.item] = o;
+    }
     B.active = false;
     return;
   }
   int qmn = 1 << 30, qmx = -(1 << 30);
   if (!e0) { qmn = 2 * B.minL1 - d - B.K0; qmx = 2 * B.maxL1 - d - B.K0; }
   if (!e1) { qmn = min(qmn, 2 * B.minL2 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL2 - (d - 1) - B.K0); }
-  if (qmx >= 2 * S - 2 || qmn <= 1) {
-    const int s_lo = (qmx - 2 * S + 4) >> 1;
-    const int s_hi = (qmn - 2) >> 1;
-    if (s_lo > s_hi) {
-      pk_save(B, d, esc);
+  if constexpr (G == 1) {
+    if (qmx >= 2 * S - 2 || qmn <= 1) {
+      const int s_lo = (qmx - 2 * S + 4) >> 1;
+      const int s_hi = (qmn - 2) >> 1;
+      if (s_lo > s_hi) {
+        pk_save<G, C>(B, gl, d, esc);
+        B.active = false;
+        return;
+      }
+      int sh = (((qmn + qmx) >> 1) - S) >> 1;
+      sh = min(max(sh, s_lo), s_hi);
+      sh = min(max(sh, -8), 8);
+      if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
+      pk_shift_n<C>(B, sh);
+      B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
+      pk_reload<G, C>(B, gl, rem, P);
+    }
+  } else {
+    int dir = 0;
+    bool ovf = false;
+    if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
+    else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
+    if (ovf) {
+      pk_save<G, C>(B, gl, d, esc);
       B.active = false;
       return;
     }
-    int sh = (((qmn + qmx) >> 1) - S) >> 1;
-    sh = min(max(sh, s_lo), s_hi);
-    sh = min(max(sh, -8), 8);
-    if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
-    pk_shift_n(B, sh);
-    B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
-    pk_reload(B, rem, P);
+    if (dir != 0) {
+      pk_shift1<G, C / 2>(B.E, gl, dir); pk_shift1<G, C / 2>(B.O, gl, dir);
+      B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
+      pk_reload<G, C>(B, gl, rem, P);
+    }
   }
 }
 
-// Run one extension per lane from its seed (item < 0: idle lane).  Warp-collective.
+// Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
+template <int G, int C>
 __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
                                        const Steal* st = nullptr) {
-  constexpr int S = 32;
-  Band16 B;
+  constexpr int S = G * C, NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
+  static_assert(S <= 32 && C % 4 == 0 && NPC <= 8, "packed window");
+  const int gl = (threadIdx.x & 31) % G;
+  Band16<G, C> B;
   if (item >= 0) {
     B.active = true; B.item = item;
     const Geom gm = item_geom(P, B.item);
@@ -326,24 +446,46 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
     B.active = false; B.item = 0;
     B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0; B.cm = 0;
   }
+  pk_keys<G, C>(B, gl, P.keym >> 8);
+  // key-byte part of the mask chains (pk_dead subtracts it)
+  uint32_t chc[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < NPC; ++j) {
+      const int u = c * NPC + j;
+      const uint32_t w = B.TC[u >> 1];
+      s = s * 2u + ((u & 1) ? ((w >> 16) & 0xffu) | (((w >> 24) & 0xffu) << 16) : (w & 0xffu) | (((w >> 8) & 0xffu) << 16));
+    }
+    chc[c] = s;
+  }
   B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) { B.E[u] = pk::DEAD2; B.O[u] = pk::DEAD2; }
-  // origin: d = 0, k = 0 -> even cell 16 = hi half of pair 0, relative to thrW_0 = BIAS - X
-  B.E[0] = (pk::DEAD2 & 0xffffu) | ((uint32_t)(32 * P.X + 15) << 16);
+  for (int u = 0; u < NP; ++u) { B.E[u] = pk::DEAD2; B.O[u] = pk::DEAD2; }
+  // origin: d = 0, k = 0 -> even cell S/2 (lane (S/2) / C, local cell (S/2) % C), relative to thrW_0 = BIAS - X
+  {
+    constexpr int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
+    if (gl == (S / 2) / C) {
+      const uint32_t v0 = (uint32_t)(32 * P.X + 31 - S / 2) & 0xffffu;
+      B.E[u0] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
+    }
+  }
   B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
   B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
   int rem = 16;
-  pk_reload(B, rem, P);
+  pk_reload<G, C>(B, gl, rem, P);
   if (B.active && B.m + B.n == 0) {
-    ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
-    P.ext[B.item] = o;
+    if (gl == 0) {
+      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+      P.ext[B.item] = o;
+    }
     B.active = false;
   }
   int d = 0, blk = 0;
   while (__any_sync(FULL, B.active)) {
-    if (st != nullptr && ((++blk & 31) == 0)) {
+    if (G == 1 && st != nullptr && ((++blk & 31) == 0)) {
       int go = 0;
       if ((threadIdx.x & 31) == 0) go = ld_volatile(st->idle) >= st->thresh;
       go = __shfl_sync(FULL, go, 0);
@@ -351,7 +493,7 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
         const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
         const int left = 2 * min(B.m - ic, B.n - (d - ic));
         if (left >= st->min_rem) {
-          pk_save(B, d, st->es);
+          pk_save<G, C>(B, gl, d, st->es);
           B.active = false;
         }
       }
@@ -360,13 +502,13 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
     const int d2 = d + 2;
     const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
     if (__any_sync(FULL, need)) {
-      pk_diag<1, true>(B, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P);
-      pk_diag<0, true>(B, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P);
+      pk_diag<G, C, 1, true>(B, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
+      pk_diag<G, C, 0, true>(B, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
     } else {
-      pk_diag<1, false>(B, d + 1, 0, 0, P);
-      pk_diag<0, false>(B, d2, 0, 0, P);
+      pk_diag<G, C, 1, false>(B, gl, d + 1, 0, 0, P, chc);
+      pk_diag<G, C, 0, false>(B, gl, d2, 0, 0, P, chc);
     }
     d = d2;
-    pk_block_end(B, d, rem, P, level, esc);
+    pk_block_end<G, C>(B, gl, d, rem, P, level, esc);
   }
 }

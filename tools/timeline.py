@@ -17,7 +17,7 @@ for ty in range(6):
     m = tl[:, 0] == ty
     if m.any():
         d = (tl[m, 3] - tl[m, 2]) / 1e6
-        print(f"  {names[ty]:6s} n={m.sum():6d} dur mean {d.mean():.2f} max {d.max():.2f} ms; "
+        print(f"  {names[ty]:6s} n={m.sum():6d} warp-ms {d.sum():9.1f} dur mean {d.mean():.2f} max {d.max():.2f} ms; "
               f"last end {(tl[m, 3].max() - t0) / 1e6:.2f} ms, last start {(tl[m, 2].max() - t0) / 1e6:.2f} ms")
 # busy warps over time
 nw = tl[:, 1].max() + 1
@@ -26,3 +26,14 @@ for a, b in zip(edges[:-1], edges[1:]):
     lo, hi = t0 + a * 1e6, t0 + b * 1e6
     busy = ((np.minimum(tl[:, 3], hi) - np.maximum(tl[:, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
     print(f"  [{a:5.1f},{b:5.1f}) ms busy warps {busy*100:5.1f}%")
+# the latest-ending work units
+if len(sys.argv) > 2:
+    o = np.argsort(-tl[:, 3])[:int(sys.argv[2])]
+    for i in o:
+        print(f"  late: {names[tl[i,0]]:6s} start {(tl[i,2]-t0)/1e6:6.2f} end {(tl[i,3]-t0)/1e6:6.2f} ms")
+    for ty in (0,):
+        m = tl[:, 0] == ty
+        d = (tl[m, 3] - tl[m, 2]) / 1e6; s = (tl[m, 2] - t0) / 1e6
+        for a in range(0, 16, 2):
+            mm = (s >= a) & (s < a + 2)
+            if mm.any(): print(f"  lane units starting [{a},{a+2}) ms: n={mm.sum()} dur mean {d[mm].mean():.2f} max {d[mm].max():.2f}")
