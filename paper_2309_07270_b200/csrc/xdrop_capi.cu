@@ -85,7 +85,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_cta = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_cta = 1;
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
@@ -128,17 +128,24 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
-  if (D.long_g == 2)
+  if (D.long_g == 2) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16, false>, 128, 0));
-  else if (D.long_g == 4)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 2, 16, true>, 128, 0));
+  } else if (D.long_g == 4) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8, false>, 128, 0));
-  if (D.long_g == 4) {
-    int o = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, xk::band_merged_kernel<32, 4, 8, true>, 128, 0));
-    D.occ_m = std::min(D.occ_m, std::max(1, o));
-  }
-  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 4, 8, true>, 128, 0));
+  } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32, false>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 1, 32, true>, 128, 0));
+  }
+  D.occ_pk = std::max(1, D.occ_pk);
+  // resident blocks per SM of the packed merged kernel: fewer co-resident warps shorten the
+  // anti-diagonal chain of the longest extensions (the launch's tail); XDROP_OCC overrides
+  {
+    const int occ_max = D.occ_pk;
+    D.occ_pk = std::min(occ_max, 2);
+    if (const char* e = getenv("XDROP_OCC")) D.occ_pk = std::max(1, std::min(occ_max, atoi(e)));
+  }
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_resume_kernel<32, 32>, 128, 0));
@@ -228,6 +235,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   P.pkM = 32 * (p.match - 2 * p.gap); P.pkU = 32 * (p.mismatch - 2 * p.gap);
   // packed 16-bit lane mode (xdrop_pk16.cuh) whenever its value range holds
   const bool pk = D.pk16 && p.xdrop + p.match <= 510;
+  const int occ = pk ? D.occ_pk : D.occ_m;   // resident blocks per SM of the merged kernel launched below
   P.ext = D.ext.as<ExtOut>();
 
   int* ctr = D.counters.as<int>();
@@ -237,7 +245,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
     xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
-                                       (long long)D.sms * D.occ_m * 128, D.long_g ? D.long_alpha : 0.f);
+                                       (long long)D.sms * occ * 128, D.long_g ? D.long_alpha : 0.f);
     xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
         D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
     launches += 3;
@@ -278,25 +286,30 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     } else {
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
                        ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
-                       (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * D.occ_m * 4 * 32), 1 << 30)};
+                       (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * occ * 4 * 32), 1 << 30)};
       if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
         CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
         mc.tl = D.tl.as<unsigned long long>(); mc.tl_cap = kTimelineCap;
       }
       // tail stealing: when 1/8 of the resident warps are idle, lane warps hand over extensions with
       // >= 1024 anti-diagonals left (a full block pool falls back to the unbounded kernel)
-      const int nwarps = D.sms * D.occ_m * 4;
+      const int nwarps = D.sms * occ * 4;
       xk::Esc es{D.pools.as<int>(), rec1, (int)caps, ctr + C_SP, D.qs.as<int>(), ctr + C_ST, gen, ctr + C_GEN};
       xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
-      if (D.long_g == 2)
-        xk::band_merged_kernel<32, 2, 16, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      const unsigned grid = (unsigned)(D.sms * occ);
+      if (D.long_g == 2 && pk)
+        xk::band_merged_kernel<32, 2, 16, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (D.long_g == 2)
+        xk::band_merged_kernel<32, 2, 16, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (D.long_g == 4 && pk)
-        xk::band_merged_kernel<32, 4, 8, true><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 4, 8, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (D.long_g == 4)
-        xk::band_merged_kernel<32, 4, 8, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 4, 8, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (pk)
+        xk::band_merged_kernel<32, 1, 32, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else
-        xk::band_merged_kernel<32, 1, 32, false><<<D.sms * D.occ_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 1, 32, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));

@@ -709,7 +709,7 @@ __device__ __forceinline__ int wait_entry(const int* q, int i) {
 #define XDROP_PK_C 32          // cells per lane of the packed lane mode
 #endif
 #ifndef XDROP_PK_MINBLOCKS
-#define XDROP_PK_MINBLOCKS 4
+#define XDROP_PK_MINBLOCKS 3
 #endif
 template <int C0, int GL, int CL, bool PK>
 __global__ void __launch_bounds__(128, PK ? XDROP_PK_MINBLOCKS : XDROP_MERGED_MINBLOCKS)
