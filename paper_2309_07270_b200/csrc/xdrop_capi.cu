@@ -90,11 +90,13 @@ struct DevCtx {
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
+  int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
+  int t0_per_sm = 2;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
   bool pk16 = true;          // packed 16-bit lane mode for T0 (XDROP_PK16=0: 32-bit lane mode)
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt;
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -143,9 +145,12 @@ int dev_open(DevCtx& D, int dev) {
   // anti-diagonal chain of the longest extensions (the launch's tail); XDROP_OCC overrides
   {
     const int occ_max = D.occ_pk;
-    D.occ_pk = std::min(occ_max, 2);
     if (const char* e = getenv("XDROP_OCC")) D.occ_pk = std::max(1, std::min(occ_max, atoi(e)));
+    if (const char* e = getenv("XDROP_T0_PER_SM")) D.t0_per_sm = std::max(0, atoi(e));
+    if (const char* e = getenv("XDROP_IDLE_NS")) D.idle_ns = std::max(0, atoi(e));
+    if (D.t0_per_sm <= 0) D.t0_per_sm = D.occ_pk;
   }
+  CKR(D.smcnt.ensure(1024 * sizeof(int)));
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_resume_kernel<32, 32>, 128, 0));
@@ -163,7 +168,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -236,6 +241,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   // packed 16-bit lane mode (xdrop_pk16.cuh) whenever its value range holds
   const bool pk = D.pk16 && p.xdrop + p.match <= 510;
   const int occ = pk ? D.occ_pk : D.occ_m;   // resident blocks per SM of the merged kernel launched below
+  const int t0b = pk ? std::min(occ, D.t0_per_sm) : occ;   // of which take fresh extensions
   P.ext = D.ext.as<ExtOut>();
 
   int* ctr = D.counters.as<int>();
@@ -245,7 +251,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
     xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
-                                       (long long)D.sms * occ * 128, D.long_g ? D.long_alpha : 0.f);
+                                       (long long)D.sms * t0b * 128, D.long_g ? D.long_alpha : 0.f);
     xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
         D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
     launches += 3;
@@ -286,14 +292,16 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     } else {
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
                        ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
-                       (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * occ * 4 * 32), 1 << 30)};
+                       (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * t0b * 4 * 32), 1 << 30),
+                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns};
+      CK(cudaMemsetAsync(D.smcnt.p, 0, 1024 * sizeof(int), s));
       if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
         CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
         mc.tl = D.tl.as<unsigned long long>(); mc.tl_cap = kTimelineCap;
       }
       // tail stealing: when 1/8 of the resident warps are idle, lane warps hand over extensions with
       // >= 1024 anti-diagonals left (a full block pool falls back to the unbounded kernel)
-      const int nwarps = D.sms * occ * 4;
+      const int nwarps = D.sms * t0b * 4;
       xk::Esc es{D.pools.as<int>(), rec1, (int)caps, ctr + C_SP, D.qs.as<int>(), ctr + C_ST, gen, ctr + C_GEN};
       xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled

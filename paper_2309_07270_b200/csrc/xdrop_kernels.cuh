@@ -653,7 +653,8 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head;
                    int* idle; int* qs_head; int* dones;
                    unsigned long long* tl; int* tl_n; int tl_cap;     // optional work-unit timeline
-                   int endgame; };                                    // T0 items left -> 4-lane dispatch
+                   int endgame;                                       // T0 items left -> 4-lane dispatch
+                   int* smcnt; int t0_per_sm; int idle_ns; };                      // blocks per SM that take T0 work
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -719,8 +720,20 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
   const int first = (GL > 1) ? n_long : 0;
+  // the first t0_per_sm resident blocks of each SM take fresh (T0) extensions; the others serve
+  // only escalated / stolen work, so T0's lane warps keep their issue share (the longest
+  // extensions' anti-diagonal chains set the launch's tail) while wide bands still find warps
+  __shared__ int s_t0;
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_t0 = (c.t0_per_sm <= 0) || atomicAdd(c.smcnt + (smid & 1023), 1) < c.t0_per_sm;
+  }
+  __syncthreads();
+  const bool t0ok = s_t0 != 0;
   bool idle = false;                    // this warp is counted in *c.idle
-  auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; };
+  unsigned nap = 1000;                  // current poll period of an escalation-only warp (ns)
+  auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; nap = 1000; };
   for (;;) {
     // T2: one checkpointed extension per warp
     {
@@ -784,7 +797,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       }
     }
     // T0: long extensions, 32/GL per warp
-    if constexpr (GL > 1) {
+    if (GL > 1 && t0ok) {
       int base = n_long;
       if (lane == 0 && ld_volatile(c.head_long) < n_long) base = atomicAdd(c.head_long, 32 / GL);
       base = __shfl_sync(FULL, base, 0);
@@ -804,7 +817,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
     // T0: the rest, 32 per warp (lane per extension); in the endgame (less than `endgame`
     // extensions left in the queue) 8 per warp with 4 lanes each, to shorten the tail
     int base = n_items, take = 32;
-    if (lane == 0) {
+    if (lane == 0 && t0ok) {
       const int h0 = first + ld_volatile(c.head0);
       if (h0 < n_items) {
         take = (n_items - h0 < c.endgame) ? 8 : 32;
@@ -844,11 +857,14 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
             fin = ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
         }
       }
-      if (!fin && !idle) { atomicAdd(c.idle, 1); idle = true; }
+      if (!fin && !idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
     }
     fin = __shfl_sync(FULL, fin, 0);
     if (fin) break;
-    __nanosleep(1000);
+    // escalation-only warps back off exponentially while their queues stay empty (their polling
+    // of the hot queue counters otherwise slows the T0 warps measurably)
+    __nanosleep(t0ok ? 1000 : nap);
+    if (!t0ok) nap = min(2 * nap, c.idle_ns);
   }
 }
 
