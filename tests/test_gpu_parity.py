@@ -301,3 +301,35 @@ def test_endgame_dispatch_exact(xd, monkeypatch):
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
     ref, rcells = oracle_of(w)
     assert_same(res, cells, ref, rcells, "endgame")
+
+
+@pytest.mark.parametrize("M,mu,g,X", [(32, -64, -64, 478), (32, -64, -64, 479), (1, -1, -1, 509),
+                                      (1, -1, -1, 510), (1, -4, -1, 15), (3, -9, -2, 40)])
+def test_packed_range_gate_and_negative_mismatch(xd, M, mu, g, X):
+    """The packed 16-bit T0 mode runs iff X + M <= 510; both sides of the gate, the
+    API's extreme scores, and schemes whose offset-space mismatch score mu - 2g is negative (the
+    borrow correction of the packed score word) stay exact."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=600 + X + M, n_pairs=150, len_lo=0, len_hi=1200, k=13, X=X,
+                                rc_frac=0.3)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X, M=M, mu=mu, g=g)
+    ref, rcells = oracle_of(w, X=X, M=M, mu=mu, g=g)
+    assert_same(res, cells, ref, rcells, f"gate M={M} mu={mu} g={g} X={X}")
+
+
+@pytest.mark.parametrize("env", [{"XDROP_PK16": "0"}, {"XDROP_OCC": "1"},
+                                 {"XDROP_T0_PER_SM": "1", "XDROP_IDLE_NS": "0"},
+                                 {"XDROP_LONG_G": "2", "XDROP_LONG_ALPHA": "0.001"}])
+def test_kernel_variants_identical(xd, env, monkeypatch):
+    """32-bit vs packed T0, 1 block/SM, 1 T0 block/SM (the rest escalation-only), packed 2-lane long
+    mode: every variant gives the oracle's results on an escalating, strand-mixed batch."""
+    from synth import workload as W
+    for k_, v in env.items():
+        monkeypatch.setenv(k_, v)
+    w = W.random_pairs_workload(seed=650, n_pairs=400, len_lo=0, len_hi=3000, k=13, X=25, rc_frac=0.4,
+                                related=0.7)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, f"variant {env}")
