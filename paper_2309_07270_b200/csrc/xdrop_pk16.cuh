@@ -229,35 +229,38 @@ __device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo,
   if constexpr (PAR == 0) kk = pk_cells<G, C, 0, CHECK>(B.E, B.O, B, gl, qlo, qhi, P, ch);
   else kk = pk_cells<G, C, 1, CHECK>(B.O, B.E, B, gl, qlo, qhi, P, ch);
   const int thr_d = B.thrN;
-  const int kmax = gmax<G>(max((int)(int16_t)(kk & 0xffffu), ((int)kk) >> 16));
-  const bool live = kmax >= 0;
+  // key maximum over both halves: both halves of kk2 hold it; the hi half sign-extends
+  const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
+  const int kmax = gmax<G>(((int)kk2) >> 16);
+  // no live cell: kmax is a dead key (< -16128), so vrel <= -505 and neither the threshold nor best
+  // can move (thrH_d = best_{<d} - X, so gv <= best - 505); no separate liveness test is needed
   const int vrel = kmax >> 5;
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
-  B.thrN = thr_d + (live ? max(0, vrel - P.X) : 0) - P.g;
-  // ---- off the critical path: live extent, best / argmax, hull count
+  B.thrN = thr_d + max(0, vrel - P.X) - P.g;
+  // ---- off the critical path: live extent, best / argmax, hull count (garbage in inactive
+  // lanes is harmless: their state is never written out)
   const uint32_t dl = pk_dead<C>(ch, chc);
   const unsigned lb = ~dl & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  const int ibase = (d + B.K0 + PAR) >> 1;
   int tmin = (__clz(lb) - (32 - C)) + C * gl;
   int tmax = (C - __ffs(lb)) + C * gl;
-  tmin = lb ? tmin : EMIN;
-  tmax = lb ? tmax : EMAX;
-  tmin = gmin<G>(tmin);
-  tmax = gmax<G>(tmax);
-  const int ibase = (d + B.K0 + PAR) >> 1;
+  tmin = gmin<G>(lb ? tmin : EMIN);
+  tmax = gmax<G>(lb ? tmax : EMAX);
+  const int mn = (tmin == EMIN) ? EMIN : ibase + tmin;
+  const int mx = (tmax == EMAX) ? EMAX : ibase + tmax;
   const int woff = -P.g * (d - B.dbase);
   const int gv = thr_d + vrel - woff;
-  const bool up = B.active && live && gv > B.best;
+  const bool up = gv > B.best;
   const int tst = 31 - (kmax & 31);
   B.best = up ? gv : B.best;
   B.istar = up ? ibase + tst : B.istar;
   B.jstar = up ? d - ibase - tst : B.jstar;
   const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
   const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
-  B.cells += (B.active && hi >= lo) ? hi - lo + 1 : 0;
+  B.cells += max(0, hi - lo + 1);
   B.minL2 = B.minL1; B.maxL2 = B.maxL1;
-  B.minL1 = (tmin == EMIN) ? EMIN : ibase + tmin;
-  B.maxL1 = (tmax == EMAX) ? EMAX : ibase + tmax;
+  B.minL1 = mn; B.maxL1 = mx;
   if constexpr (PAR == 0) {       // even -> odd: a advances
     B.A0 = __funnelshift_r(B.A0, B.An0, 1); B.A1 = __funnelshift_r(B.A1, B.An1, 1);
     B.An0 >>= 1; B.An1 >>= 1;
