@@ -85,7 +85,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_cta = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1;
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
@@ -154,6 +154,8 @@ int dev_open(DevCtx& D, int dev) {
   D.occ_m = std::max(1, D.occ_m);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l1, xk::band_kernel<32, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_l2, xk::band_resume_kernel<32, 32>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk2, xk::pk_resume_kernel<32, 32>, 128, 0));
+  D.occ_pk2 = std::max(1, D.occ_pk2);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_gen, xk::general_kernel, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta, xk::band_cta_kernel<256, 16>, 256, 0));
   D.occ_cta = std::max(1, D.occ_cta);
@@ -328,7 +330,10 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
     } else {
-      xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
+      if (pk)
+        xk::pk_resume_kernel<32, 32><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
+      else
+        xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
       xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e4, ctr + C_HEAD4, eg, 2);
       launches += 2;
     }

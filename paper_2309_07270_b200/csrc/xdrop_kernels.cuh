@@ -649,6 +649,25 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 
 #include "xdrop_pk16.cuh"
 
+// Standalone kernel resuming checkpointed extensions in the packed 16-bit mode (X + M <= 510).
+template <int G, int C>
+__global__ void __launch_bounds__(128)
+pk_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
+  constexpr int IPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int n = *src.q_tail;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(queue_head, IPW);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= n) break;
+    const int slot = base + grp;
+    const int* rec = slot < n ? src.pool + (size_t)src.q[slot] * src.rec_ints : nullptr;
+    pk_resume<G, C>(P, rec, level, esc);
+  }
+}
+
 // Counters of the merged kernel (ints): see xdrop_capi.cu
 struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_head; int* done1; int* q2_head;
                    int* idle; int* qs_head; int* dones;
@@ -747,7 +766,8 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         slot = __shfl_sync(FULL, slot, 0);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        if constexpr (PK) pk_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        else band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
         tl_rec(c, 4, t0);
         continue;
       }
@@ -767,7 +787,8 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         slot = __shfl_sync(FULL, slot, lane & ~7);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        if constexpr (PK) pk_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        else band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
         tl_rec(c, 3, t0);
         __threadfence();
         __syncwarp();
@@ -788,7 +809,8 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         slot = __shfl_sync(FULL, slot, lane & ~3);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        band_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        if constexpr (PK) pk_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        else band_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
         tl_rec(c, 2, t0);
         __threadfence();
         __syncwarp();

@@ -94,7 +94,8 @@ template <int G, int C> struct Band16 {
 template <int G, int C>
 __device__ __forceinline__ void pk_keys(Band16<G, C>& B, int gl, int zero) {
   constexpr int NP = C / 2;
-  const int tb = 31 - C * gl + zero;
+  const int tb = 31 + zero;                       // key bytes 31 - (local cell); G > 1 breaks ties by lane
+  (void)gl;
 #pragma unroll
   for (int j = 0; j < NP / 2; ++j)
     B.TC[j] = opaque((uint32_t)(tb - 2 * j) | ((uint32_t)(tb - 2 * j - NP) << 8) |
@@ -231,10 +232,22 @@ __device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo,
   const int thr_d = B.thrN;
   // key maximum over both halves: both halves of kk2 hold it; the hi half sign-extends
   const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
-  const int kmax = gmax<G>(((int)kk2) >> 16);
+  const int kl = ((int)kk2) >> 16;                        // lane key: 32 * value + 31 - (local cell)
   // no live cell: kmax is a dead key (< -16128), so vrel <= -505 and neither the threshold nor best
   // can move (thrH_d = best_{<d} - X, so gv <= best - 505); no separate liveness test is needed
-  const int vrel = kmax >> 5;
+  int vrel, tst;
+  if constexpr (G == 1) {
+    vrel = kl >> 5;
+    tst = 31 - (kl & 31);
+  } else {                                                // value first, then the lowest lane, then t
+    const int vl = kl >> 5;
+    vrel = gmax<G>(vl);
+    const unsigned ball = __ballot_sync(FULL, vl == vrel);
+    const int grp = (threadIdx.x & 31) / G;
+    const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
+    const int first = __ffs(gb) - 1;
+    tst = __shfl_sync(FULL, C * gl + 31 - (kl & 31), first, G);
+  }
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
   B.thrN = thr_d + max(0, vrel - P.X) - P.g;
@@ -252,7 +265,6 @@ __device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo,
   const int woff = -P.g * (d - B.dbase);
   const int gv = thr_d + vrel - woff;
   const bool up = gv > B.best;
-  const int tst = 31 - (kmax & 31);
   B.best = up ? gv : B.best;
   B.istar = up ? ibase + tst : B.istar;
   B.jstar = up ? d - ibase - tst : B.jstar;
@@ -432,26 +444,10 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
   }
 }
 
-// Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
+// key-byte part of the PRMT-mask chains (pk_dead subtracts it)
 template <int G, int C>
-__device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
-                                       const Steal* st = nullptr) {
-  constexpr int S = G * C, NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
-  static_assert(S <= 32 && C % 4 == 0 && NPC <= 8, "packed window");
-  const int gl = (threadIdx.x & 31) % G;
-  Band16<G, C> B;
-  if (item >= 0) {
-    B.active = true; B.item = item;
-    const Geom gm = item_geom(P, B.item);
-    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
-    B.cm = (uint32_t)gm.bmask;
-  } else {
-    B.active = false; B.item = 0;
-    B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0; B.cm = 0;
-  }
-  pk_keys<G, C>(B, gl, P.keym >> 8);
-  // key-byte part of the mask chains (pk_dead subtracts it)
-  uint32_t chc[NCH];
+__device__ __forceinline__ void pk_chain_consts(const Band16<G, C>& B, uint32_t (&chc)[C > 16 ? 2 : 1]) {
+  constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     uint32_t s = 0;
@@ -463,30 +459,17 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
     }
     chc[c] = s;
   }
-  B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1;
-#pragma unroll
-  for (int u = 0; u < NP; ++u) { B.E[u] = pk::DEAD2; B.O[u] = pk::DEAD2; }
-  // origin: d = 0, k = 0 -> even cell S/2 (lane (S/2) / C, local cell (S/2) % C), relative to thrW_0 = BIAS - X
-  {
-    constexpr int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
-    if (gl == (S / 2) / C) {
-      const uint32_t v0 = (uint32_t)(32 * P.X + 31 - S / 2) & 0xffffu;
-      B.E[u0] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
-    }
-  }
-  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
-  B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;
-  B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
-  int rem = 16;
+}
+
+// anti-diagonal loop (from an even d; groups of a warp may sit at different d)
+template <int G, int C>
+__device__ __forceinline__ void pk_loop(Band16<G, C>& B, int gl, int d, const Problem& P, int level, const Esc& esc,
+                                        const Steal* st) {
+  constexpr int S = G * C;
+  uint32_t chc[C > 16 ? 2 : 1];
+  pk_chain_consts<G, C>(B, chc);
+  int rem = 16, blk = 0;
   pk_reload<G, C>(B, gl, rem, P);
-  if (B.active && B.m + B.n == 0) {
-    if (gl == 0) {
-      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
-      P.ext[B.item] = o;
-    }
-    B.active = false;
-  }
-  int d = 0, blk = 0;
   while (__any_sync(FULL, B.active)) {
     if (G == 1 && st != nullptr && ((++blk & 31) == 0)) {
       int go = 0;
@@ -514,4 +497,112 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
     d = d2;
     pk_block_end<G, C>(B, gl, d, rem, P, level, esc);
   }
+}
+
+template <int G, int C>
+__device__ __forceinline__ void pk_geom(Band16<G, C>& B, const Problem& P, int item) {
+  if (item >= 0) {
+    B.active = true; B.item = item;
+    const Geom gm = item_geom(P, B.item);
+    B.sa = gm.sa; B.sb = gm.sb; B.da = gm.da; B.db = gm.db; B.m = gm.m; B.n = gm.n;
+    B.cm = (uint32_t)gm.bmask;
+  } else {
+    B.active = false; B.item = 0;
+    B.sa = GUARD; B.sb = GUARD; B.da = 1; B.db = 1; B.m = 0; B.n = 0; B.cm = 0;
+  }
+}
+
+// Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
+template <int G, int C>
+__device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
+                                       const Steal* st = nullptr) {
+  constexpr int S = G * C, NP = C / 2;
+  static_assert(S <= 32 && C % 4 == 0 && NP <= 16, "packed window from a seed");
+  const int gl = (threadIdx.x & 31) % G;
+  Band16<G, C> B;
+  pk_geom<G, C>(B, P, item);
+  pk_keys<G, C>(B, gl, P.keym >> 8);
+  B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1;
+#pragma unroll
+  for (int u = 0; u < NP; ++u) { B.E[u] = pk::DEAD2; B.O[u] = pk::DEAD2; }
+  // origin: d = 0, k = 0 -> even cell S/2 (lane (S/2) / C, local cell tl), relative to thrW_0 = BIAS - X
+  {
+    constexpr int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
+    if (gl == (S / 2) / C) {
+      const uint32_t v0 = (uint32_t)(32 * P.X + 31 - tl) & 0xffffu;
+      B.E[u0] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
+    }
+  }
+  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
+  B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;
+  B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
+  if (B.active && B.m + B.n == 0) {
+    if (gl == 0) {
+      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+      P.ext[B.item] = o;
+    }
+    B.active = false;
+  }
+  pk_loop<G, C>(B, gl, 0, P, level, esc, st);
+}
+
+// Resume one checkpointed extension per group (rec == nullptr: idle group) from a 32-bit record
+// (band_save / pk_save format) in a window of S = G*C >= the record's; the old window lands in the
+// middle.  Stored values become relative to a reference T per anti-diagonal with every live W >= T
+// and W - T <= X + M:  T_d = min(thrW_{d+1} + g, min live W_d), T_{d-1} = min(thrW_{d+1} + 2g, min
+// live W_{d-1}) (the true thresholds satisfy thr_d <= thrW_{d+1} + g, thr_{d-1} <= thr_d + g, and
+// live values exceed their threshold by at most X + M).  The recurrence only needs differences of
+// the references, so any such T is exact.
+template <int G, int C>
+__device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int level, const Esc& esc) {
+  constexpr int S = G * C, NP = C / 2;
+  const int gl = (threadIdx.x & 31) % G;
+  Band16<G, C> B;
+  int d = 0;
+  pk_geom<G, C>(B, P, rec ? rec[0] : -1);
+  pk_keys<G, C>(B, gl, P.keym >> 8);
+  int w_e[C], w_o[C];                                    // this lane's cells: even (d), odd (d-1)
+  if (rec) {
+    d = rec[1];
+    const int s_src = rec[14];
+    const int sh = S - s_src;                            // K0' = K0 - sh (sh >= 0, even)
+    B.K0 = rec[2] - sh; B.dbase = rec[3]; B.thrN = rec[4]; B.best = rec[5];
+    B.istar = rec[6]; B.jstar = rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
+    B.maxL2 = rec[11]; B.ia0 = rec[12] - sh / 2; B.jb0 = rec[13] + sh / 2;
+    B.cells = rec[15];
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int qe = 2 * (C * gl + t) - sh, qo = qe + 1;
+      w_e[t] = (qe >= 0 && qe < 2 * s_src) ? rec[HDR + qe] : NEGV;
+      w_o[t] = (qo >= 0 && qo < 2 * s_src) ? rec[HDR + qo] : NEGV;
+    }
+  } else {
+    B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1; B.dbase = 0; B.thrN = 0; B.best = 0;
+    B.istar = 0; B.jstar = 0; B.cells = 0; B.minL1 = EMIN; B.maxL1 = EMAX; B.minL2 = EMIN; B.maxL2 = EMAX;
+#pragma unroll
+    for (int t = 0; t < C; ++t) { w_e[t] = NEGV; w_o[t] = NEGV; }
+  }
+  int me = 1 << 30, mo = 1 << 30;                        // live W > 0 (biased); dead cells are negative
+#pragma unroll
+  for (int t = 0; t < C; ++t) {
+    if (w_e[t] > 0) me = min(me, w_e[t]);
+    if (w_o[t] > 0) mo = min(mo, w_o[t]);
+  }
+  me = gmin<G>(me); mo = gmin<G>(mo);
+  B.thrD = min(B.thrN + P.g, me);
+  B.thrD1 = min(B.thrN + 2 * P.g, mo);
+#pragma unroll
+  for (int u = 0; u < NP; ++u) {
+    uint32_t e = 0, o = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = u + NP * h;
+      const uint32_t tc = 31 - t;
+      const uint32_t ve = w_e[t] > 0 ? ((uint32_t)(32 * (w_e[t] - B.thrD)) | tc) & 0xffffu : 0xC000u | tc;
+      const uint32_t vo = w_o[t] > 0 ? ((uint32_t)(32 * (w_o[t] - B.thrD1)) | tc) & 0xffffu : 0xC000u | tc;
+      e |= ve << (16 * h); o |= vo << (16 * h);
+    }
+    B.E[u] = e; B.O[u] = o;
+  }
+  pk_loop<G, C>(B, gl, d, P, level, esc, nullptr);
 }

@@ -333,3 +333,16 @@ def test_kernel_variants_identical(xd, env, monkeypatch):
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
     ref, rcells = oracle_of(w)
     assert_same(res, cells, ref, rcells, f"variant {env}")
+
+
+def test_packed_resume_reaches_s1024(xd):
+    """Unrelated continuations at X = 400 (packed path: X + M <= 510) outgrow T0 (32 cells), T1 (64)
+    and T2 (256): checkpoints resume in the packed 16-bit tiers up to the S = 1024 kernel, exactly."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=660, n_pairs=24, len_lo=2500, len_hi=4000, k=11, X=400, related=0.0)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, "packed resume S1024")
+    assert st["escalated"][2] > 0, st["escalated"]
