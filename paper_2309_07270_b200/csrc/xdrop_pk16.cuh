@@ -34,6 +34,10 @@
 // (xdrop_capi.cu falls back to the 32-bit lane mode otherwise).
 #pragma once
 
+#ifndef XDROP_PK_FMA
+#define XDROP_PK_FMA 1           // cell adds on the FMA pipe (see pk_cells)
+#endif
+
 namespace pk {
 constexpr uint32_t DEAD2 = 0xC000C000u;    // a pair of dead cells
 constexpr uint32_t KILLC = 0xC01FC01Fu;    // LOP3 constant: bits taken from the PRMT mask
@@ -141,7 +145,7 @@ __device__ __forceinline__ uint32_t tree16(const uint32_t (&k)[N]) {
 // One anti-diagonal d of parity PAR: V (parity PAR, holds d-2) is updated in place from
 // N (holds d-1).  CHECK: cells with q outside [qlo, qhi] (beyond the matrix) are dead.
 // Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
-template <int G, int C, int PAR, bool CHECK>
+template <int G, int C, int PAR, bool CHECK, bool FMA = (XDROP_PK_FMA != 0)>
 __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<G, C>& B,
                                              int gl, int qlo, int qhi, const Problem& P, uint32_t (&ch)[C > 16 ? 2 : 1]) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
@@ -160,6 +164,8 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
     mis = (mis & LO) | ((mis << (16 - NP)) & (LO << 16));
   }
   const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
+  const uint32_t one = two >> 1;                          // 1, opaque: keeps the adds on IMAD
+  (void)one;
   // seam pair: the neighbour cell beyond the lane's last (first) cell
   uint32_t seam;
   if constexpr (PAR == 0) {
@@ -171,6 +177,9 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
     if constexpr (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
     seam = __byte_perm(N[0], x, 0x5432);                 // (own even cell NP, right lane's even cell 0)
   }
+  // the hi half of a seam pair may hold a cell with key bits up to 31 (the next lane's cell 0);
+  // clear them so the FMA-pipe adds' carries (see below) cannot reach its value bits
+  if constexpr (G > 1 && FMA) seam &= 0xFFE0FFFFu;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) ch[c] = 0;
 #pragma unroll
@@ -183,11 +192,21 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
       L = N[u];
       R = (u == NP - 1) ? seam : N[u == NP - 1 ? 0 : u + 1];
     }
-    const uint32_t nb = __vmaxs2(L, R);
     const uint32_t sh = (u == 0) ? mis : __umulhi(mis, 1u << (32 - u));
     const uint32_t sE = (sh & 0x00010001u) * kk + base;
-    uint32_t v = __viaddmax_s16x2(V[u], sE, nb);
+    uint32_t v;
+    if constexpr (FMA) {
+    // the two adds as 32-bit IMADs (FMA pipe) instead of 16x2 ALU ops: a carry out of the low
+    // half adds 1 to the high half, i.e. to the key bits of a hi cell (31 - t <= 31 - NP <= 27),
+    // at most +2 over both adds, so it never reaches the value bits; the kill rewrites the keys
+    const uint32_t X2 = V[u] * one + sE;
+    v = __vimax3_s16x2(L, R, X2);
+    v = v * one + D1p;
+    } else {
+    const uint32_t nb = __vmaxs2(L, R);
+    v = __viaddmax_s16x2(V[u], sE, nb);
     v = __viaddmax_s16x2(v, D1p, pk::NOFLOOR);
+    }
     if constexpr (CHECK) {
       const int q0 = 2 * (C * gl + u) + PAR, q1 = q0 + 2 * NP;
       const uint32_t cap = ((q0 >= qlo && q0 <= qhi) ? 0x7FFFu : 0x8000u) |
@@ -340,6 +359,15 @@ __device__ __forceinline__ void pk_shift1(uint32_t (&A)[NP], int gl, int dir) {
   }
 }
 
+// after a window shift: restore the key bits 31 - (local cell) of every pair (a shift moves lo
+// cells, whose keys reach 31, into hi halves, where the FMA-pipe adds may carry into the keys)
+template <int NP>
+__device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP]) {
+#pragma unroll
+  for (int u = 0; u < NP; ++u)
+    A[u] = (A[u] & 0xFFE0FFE0u) | (uint32_t)(31 - u) | ((uint32_t)(31 - u - NP) << 16);
+}
+
 // checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
 template <int G, int C>
 __device__ __forceinline__ void pk_save(const Band16<G, C>& B, int gl, int d, const Esc& e) {
@@ -423,6 +451,7 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
       sh = min(max(sh, -8), 8);
       if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
       pk_shift_n<C>(B, sh);
+      pk_rekey<C / 2>(B.E); pk_rekey<C / 2>(B.O);
       B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
       pk_reload<G, C>(B, gl, rem, P);
     }
@@ -438,6 +467,7 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
     }
     if (dir != 0) {
       pk_shift1<G, C / 2>(B.E, gl, dir); pk_shift1<G, C / 2>(B.O, gl, dir);
+      pk_rekey<C / 2>(B.E); pk_rekey<C / 2>(B.O);
       B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
       pk_reload<G, C>(B, gl, rem, P);
     }
