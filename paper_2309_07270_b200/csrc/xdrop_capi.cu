@@ -91,7 +91,7 @@ struct DevCtx {
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
-  int t0_per_sm = 2;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
+  int t0_per_sm = 3;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
   bool pk16 = true;          // packed 16-bit lane mode for T0 (XDROP_PK16=0: 32-bit lane mode)
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
