@@ -136,6 +136,25 @@ int xdrop_align_batch_device(xdrop_ctx* ctx,
                              const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
                              xdrop_result* out, int64_t* cells_out, void* stream);
 
+/* ---- several seeds per candidate pair (reading Q26) ----
+ * Seed-and-extend tools extend every seed a candidate pair shares and keep the best alignment
+ * ("seed-and-extend").  A candidate is a maximal run of ADJACENT rows
+ * of `pairs` with equal a_id and equal b_id (the strand bit XDROP_PAIR_RC included); non-adjacent
+ * repeats are separate candidates.  best[i] = the index of the row of i's candidate with the
+ * highest score, ties to the lowest index.
+ *
+ * Device form: pairs (n x 16 B), res (n x 20 B, e.g. the `out` of xdrop_align_batch_device) and
+ * best (n x int64) are device pointers; work is enqueued on `stream` (NULL = the context's
+ * stream) and the call returns after the stream has completed.  n = 0 is a no-op; n < 0 or a NULL
+ * pointer with n > 0 -> XDROP_EINVAL. */
+int xdrop_best_seed_device(xdrop_ctx* ctx, const xdrop_pair* pairs, const xdrop_result* res, int64_t n,
+                           int64_t* best, void* stream);
+/* Host form: xdrop_align_batch (out, cells_out as there) + the selection above into best
+ * (n_pairs x int64, caller-owned host memory). */
+int xdrop_align_multiseed(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
+                          const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                          xdrop_result* out, int64_t* best, int64_t* cells_out);
+
 /* Counters of the last call on this context (first device). */
 typedef struct {
   int64_t items;          /* extensions (2 per pair) */

@@ -134,3 +134,24 @@ def align_batch(seqA: np.ndarray, offA: np.ndarray, seqB: np.ndarray, offB: np.n
     if rc:
         raise ValueError(f"oracle_align_batch failed rc={rc} at pair {err.value}")
     return out, cells
+
+
+def best_seed(pairs: np.ndarray, scores: np.ndarray) -> np.ndarray:
+    """Several seeds per candidate pair (reading Q26): a candidate
+    is a maximal run of adjacent rows with equal (a_id, b_id) (strand bit included); every row
+    gets the index of its candidate's highest-scoring row, ties to the first.  Plain loop."""
+    pairs = np.asarray(pairs).reshape(-1, 4)
+    n = pairs.shape[0]
+    best = np.zeros(n, dtype=np.int64)
+    i = 0
+    while i < n:
+        j = i
+        while j + 1 < n and pairs[j + 1, 0] == pairs[i, 0] and pairs[j + 1, 1] == pairs[i, 1]:
+            j += 1
+        b = i
+        for t in range(i + 1, j + 1):
+            if scores[t] > scores[b]:
+                b = t
+        best[i:j + 1] = b
+        i = j + 1
+    return best

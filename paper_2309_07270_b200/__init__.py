@@ -103,6 +103,40 @@ class Aligner:
             cells.data_ptr() if cells is not None else None, s)
         N.check(st, "xdrop_align_batch_device", self._h)
 
+    # ------------------------------------------------- several seeds per pair (f4)
+    def align_multiseed(self, seqA: np.ndarray, offA: np.ndarray, pairs: np.ndarray, k: int, X: int,
+                        M: int = 1, mu: int = -1, g: int = -1, seqB=None, offB=None):
+        """xdrop_align_multiseed: every row aligned as by align(), plus best int64[n] = the row of
+        each row's candidate (adjacent rows with equal a_id, b_id) with the highest score."""
+        seqA = np.ascontiguousarray(seqA, dtype=np.uint8)
+        offA = np.ascontiguousarray(offA, dtype=np.int64)
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 4)
+        A = N.Seqs(seqA.ctypes.data, offA.ctypes.data, offA.shape[0] - 1)
+        if seqB is None:
+            pB = ctypes.byref(A)
+        else:
+            seqB = np.ascontiguousarray(seqB, dtype=np.uint8)
+            offB = np.ascontiguousarray(offB, dtype=np.int64)
+            B = N.Seqs(seqB.ctypes.data, offB.ctypes.data, offB.shape[0] - 1)
+            pB = ctypes.byref(B)
+        n = pairs.shape[0]
+        out = np.zeros(n, dtype=RESULT_DTYPE)
+        cells = np.zeros(n, dtype=np.int64)
+        best = np.zeros(n, dtype=np.int64)
+        p = _params(M, mu, g, X, k)
+        st = N.lib.xdrop_align_multiseed(self._h, ctypes.byref(A), pB, pairs.ctypes.data, n, ctypes.byref(p),
+                                         out.ctypes.data, best.ctypes.data, cells.ctypes.data)
+        N.check(st, "xdrop_align_multiseed", self._h)
+        return out, best, cells
+
+    def best_seed_device(self, pairs, out, best, stream=None):
+        """xdrop_best_seed_device on torch CUDA tensors: pairs int32[n,4], out int32[n,5] (as
+        written by align_device), best int64[n]."""
+        s = stream.cuda_stream if stream is not None else None
+        st = N.lib.xdrop_best_seed_device(self._h, pairs.data_ptr(), out.data_ptr(), pairs.shape[0],
+                                          best.data_ptr(), s)
+        N.check(st, "xdrop_best_seed_device", self._h)
+
     # ------------------------------------------------------------ observability
     def stats(self) -> dict:
         s = N.Stats()

@@ -63,6 +63,7 @@ TRACE_DTYPE = np.dtype([("rank", "<i4"), ("gpu", "<i4"), ("batch", "<i4"), ("sub
 
 EXPORTS = [
     "xdrop_init", "xdrop_align_batch", "xdrop_align_batch_device", "xdrop_last_stats",
+    "xdrop_best_seed_device", "xdrop_align_multiseed",
     "xdrop_last_sched_stats", "xdrop_last_trace", "xdrop_sched_simulate", "xdrop_ring_left",
     "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_int32_peak",
     "xdrop_last_timeline",
@@ -81,6 +82,9 @@ def _load():
     lib.xdrop_align_batch_device.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int64, P, P, ctypes.c_int64,
                                              ctypes.c_int64, P, ctypes.c_int64, ctypes.POINTER(Params), P, P, P]
     lib.xdrop_last_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    lib.xdrop_best_seed_device.argtypes = [P, P, P, ctypes.c_int64, P, P]
+    lib.xdrop_align_multiseed.argtypes = [P, ctypes.POINTER(Seqs), ctypes.POINTER(Seqs), P, ctypes.c_int64,
+                                          ctypes.POINTER(Params), P, P, P]
     lib.xdrop_last_sched_stats.argtypes = [P, ctypes.POINTER(SchedStats)]
     lib.xdrop_last_trace.argtypes = [P, P, ctypes.c_int64]
     lib.xdrop_last_trace.restype = ctypes.c_int64

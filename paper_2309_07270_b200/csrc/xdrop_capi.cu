@@ -96,7 +96,7 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best;
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -170,7 +170,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -519,6 +519,24 @@ extern "C" int xdrop_align_batch_device(xdrop_ctx* ctx, const char* seqA, const 
   return rc;
 }
 
+// f4: best seed per candidate (device pointers)
+extern "C" int xdrop_best_seed_device(xdrop_ctx* ctx, const xdrop_pair* pairs, const xdrop_result* res, int64_t n,
+                                      int64_t* best, void* stream) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  if (n < 0 || (n > 0 && (!pairs || !res || !best))) return XDROP_EINVAL;
+  if (n == 0) return 0;
+  DevCtx& D = ctx->devs[0];
+  CK(cudaSetDevice(D.dev));
+  cudaStream_t s = stream ? (cudaStream_t)stream : D.stream;
+  xk::best_seed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const PairDesc*>(pairs), reinterpret_cast<const int*>(res), n,
+      reinterpret_cast<long long*>(best));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 // ---------------------------------------------------------------- host API
 namespace {
 
@@ -744,5 +762,30 @@ extern "C" int xdrop_int32_peak(xdrop_ctx* ctx, double* ops_per_s) {
     const double ops = (double)blocks * threads * iters * 16.0 * 16.0;
     ops_per_s[mode] = ops / (best * 1e-3);
   }
+  return 0;
+}
+
+// f4 host form: the batch, then the selection kernel on the first device
+extern "C" int xdrop_align_multiseed(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
+                                     const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                                     xdrop_result* out, int64_t* best, int64_t* cells_out) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  if (n_pairs > 0 && !best) return XDROP_EINVAL;
+  int rc = xdrop_align_batch(ctx, A, B, pairs, n_pairs, p, out, cells_out);
+  if (rc || n_pairs == 0) return rc;
+  DevCtx& D = ctx->devs[0];
+  CK(cudaSetDevice(D.dev));
+  cudaStream_t s = D.stream;
+  CKR(D.ms_pairs.ensure((size_t)n_pairs * sizeof(xdrop_pair)));
+  CKR(D.ms_res.ensure((size_t)n_pairs * sizeof(xdrop_result)));
+  CKR(D.ms_best.ensure((size_t)n_pairs * sizeof(int64_t)));
+  CK(cudaMemcpyAsync(D.ms_pairs.p, pairs, (size_t)n_pairs * sizeof(xdrop_pair), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(D.ms_res.p, out, (size_t)n_pairs * sizeof(xdrop_result), cudaMemcpyHostToDevice, s));
+  rc = xdrop_best_seed_device(ctx, reinterpret_cast<const xdrop_pair*>(D.ms_pairs.p),
+                              reinterpret_cast<const xdrop_result*>(D.ms_res.p), n_pairs,
+                              reinterpret_cast<int64_t*>(D.ms_best.p), s);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(best, D.ms_best.p, (size_t)n_pairs * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return 0;
 }

@@ -1315,6 +1315,29 @@ __global__ void combine_kernel(Problem P, int* __restrict__ out5, long long* __r
 }
 
 // ----------------------------------------------------- INT32 issue-rate probe
+// f4: best seed per candidate (adjacent rows with equal a_id, b_id); the thread of a candidate's
+// first row scans the run once (O(n) total), ties to the lowest row
+__global__ void best_seed_kernel(const PairDesc* __restrict__ pairs, const int* __restrict__ res5, int64_t n,
+                                 long long* __restrict__ best) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const PairDesc p = pairs[i];
+  if (i > 0) {
+    const PairDesc q = pairs[i - 1];
+    if (q.a_id == p.a_id && q.b_id == p.b_id) return;      // not the first row of its candidate
+  }
+  int64_t j = i, bi = i;
+  int bs = res5[5 * i];
+  while (j + 1 < n) {
+    const PairDesc q = pairs[j + 1];
+    if (q.a_id != p.a_id || q.b_id != p.b_id) break;
+    ++j;
+    const int s = res5[5 * j];
+    if (s > bs) { bs = s; bi = j; }
+  }
+  for (int64_t t = i; t <= j; ++t) best[t] = bi;
+}
+
 template <bool DUAL>
 __global__ void int32_peak_kernel(int iters, int seed, int* sink) {
   int a0 = threadIdx.x + seed, a1 = a0 ^ 0x55, a2 = a0 * 3, a3 = a0 + 7;

@@ -122,10 +122,13 @@ def _choose_seed(rng, sa, ca, sb, cb, k):
 def make_pool_workload(name: str, seed: int, genome_len: int, n_pairs: int, length_sampler,
                        coverage: float, min_ov: int, k: int = 17, X: int = 15,
                        sub: float = 0.015, ins: float = 0.09, dele: float = 0.045,
-                       f_sp: float = 0.0, max_reads: Optional[int] = None, rc_frac: float = 0.0) -> Workload:
+                       f_sp: float = 0.0, max_reads: Optional[int] = None, rc_frac: float = 0.0,
+                       seeds_per_pair: int = 1) -> Workload:
     """Pool mode: reads from one genome; pairs are overlapping reads (plus spurious).
     rc_frac: fraction of reads sequenced from the reverse strand (stored reverse-
-    complemented); pairs of reads from opposite strands carry XDROP_PAIR_RC."""
+    complemented); pairs of reads from opposite strands carry XDROP_PAIR_RC.
+    seeds_per_pair > 1: each overlapping pair gets that many independently drawn seeds, as
+    adjacent rows (the candidate layout of xdrop_align_multiseed); n_pairs counts candidates."""
     rng = np.random.default_rng(seed)
     genome = rng.integers(0, 4, size=genome_len, dtype=np.uint8)
     mean_len = float(np.mean(length_sampler(rng, 4096)))
@@ -156,7 +159,7 @@ def make_pool_workload(name: str, seed: int, genome_len: int, n_pairs: int, leng
     perm = rng.permutation(cand_i.shape[0])
     pairs = []
     for t in perm:
-        if len(pairs) >= n_true:
+        if len(pairs) >= n_true * seeds_per_pair:
             break
         i, j = int(cand_i[t]), int(cand_j[t])
         if rng.random() < 0.5:
@@ -165,6 +168,9 @@ def make_pool_workload(name: str, seed: int, genome_len: int, n_pairs: int, leng
         if p is None:
             continue
         pairs.append((i, j, int(rpos[i][p - starts[i]]), int(rpos[j][p - starts[j]])))
+        for _ in range(seeds_per_pair - 1):
+            p = _choose_seed(rng, int(starts[i]), clean[i], int(starts[j]), clean[j], k)
+            pairs.append((i, j, int(rpos[i][p - starts[i]]), int(rpos[j][p - starts[j]])))
     extra = []
     tries = 0
     while len(extra) < n_sp and tries < 100 * max(1, n_sp):
