@@ -267,7 +267,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     const int64_t cap1 = std::min<int64_t>(n_items, 1 << 20), cap2 = std::min<int64_t>(n_items, 1 << 18),
                   cap3 = std::min<int64_t>(n_items, 1 << 17);
     const int64_t cap4 = std::min<int64_t>(n_items, 1 << 14);
-    const int rec1 = xk::HDR + 2 * 32, rec2 = xk::HDR + 2 * 64, rec3 = xk::HDR + 2 * 256, rec4 = xk::HDR + 2 * 1024;
+    // record sizes hold the source tier's window: T0 32, T1 64 (32-bit) / 128 (packed), T2 256, S1024
+    const int rec1 = xk::HDR + 2 * 32, rec2 = xk::HDR + 2 * 128, rec3 = xk::HDR + 2 * 256, rec4 = xk::HDR + 2 * 1024;
     CKR(D.pool1.ensure((size_t)std::max<int64_t>(cap1, 1) * rec1 * sizeof(int)));
     CKR(D.pool2.ensure((size_t)std::max<int64_t>(cap2, 1) * rec2 * sizeof(int)));
     CKR(D.pool3.ensure((size_t)std::max<int64_t>(cap3, 1) * rec3 * sizeof(int)));

@@ -725,6 +725,19 @@ __device__ __forceinline__ int wait_entry(const int* q, int i) {
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
+// packed T1 / T2 shapes.  Measured (E. coli, C. elegans x0.05, X-sweep): the escalation tiers are
+// latency-bound (their extensions escalated late and run alone), so few cells per lane win:
+// T1 8 x 8 (S = 64) and T2 32 x 8 (S = 256, one per warp) beat 8 x 16 / 16 x 8 (S = 128) and
+// 16 x 16 (two per warp) everywhere except X = 100
+#ifndef XDROP_T1_G
+#define XDROP_T1_G 8
+#endif
+#ifndef XDROP_T1_C
+#define XDROP_T1_C 8
+#endif
+#ifndef XDROP_T2_G
+#define XDROP_T2_G 32
+#endif
 #ifndef XDROP_PK_C
 #define XDROP_PK_C 32          // cells per lane of the packed lane mode
 #endif
@@ -754,40 +767,44 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
   unsigned nap = 1000;                  // current poll period of an escalation-only warp (ns)
   auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; nap = 1000; };
   for (;;) {
-    // T2: one checkpointed extension per warp
+    // T2 (S = 256): 32 / XDROP_T2_G extensions per warp (packed), one per warp (32-bit)
     {
+      constexpr int W2 = PK ? 32 / XDROP_T2_G : 1;
       int k = 0, h = 0;
-      if (lane == 0) h = claim(c.q2_head, e2.q_tail, 1, true, k);
+      if (lane == 0) h = claim(c.q2_head, e2.q_tail, W2, true, k);
       k = __shfl_sync(FULL, k, 0);
       if (k) {
         h = __shfl_sync(FULL, h, 0);
-        int slot = 0;
-        if (lane == 0) slot = wait_entry(e2.q, h);
-        slot = __shfl_sync(FULL, slot, 0);
+        const int g = lane / (32 / W2);
+        int slot = -1;
+        if (g < k && (lane % (32 / W2)) == 0) slot = wait_entry(e2.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~(32 / W2 - 1));
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        if constexpr (PK) pk_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
-        else band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        const int* rec = slot >= 0 ? e2.pool + (size_t)slot * e2.rec_ints : nullptr;
+        if constexpr (PK) pk_resume<XDROP_T2_G, 256 / XDROP_T2_G>(P, rec, 1, e3);
+        else band_resume<32, 8>(P, rec, 1, e3);
         tl_rec(c, 4, t0);
         continue;
       }
     }
-    // T1: up to 4 checkpointed extensions per warp, eight lanes x 8 cells each (S = 64),
+    // T1: up to 4 checkpointed extensions per warp, eight lanes x 8 cells (S = 64),
     // claimed as soon as they appear: few extensions get here and each one escalated late in
     // its life, so a short per-anti-diagonal latency matters more than full lanes
     {
+      constexpr int G1 = PK ? XDROP_T1_G : 8, W1 = 32 / G1;
       int k = 0, h = 0;
-      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 4, true, k);
+      if (lane == 0) h = claim(c.q1_head, e1.q_tail, W1, true, k);
       k = __shfl_sync(FULL, k, 0);
       if (k) {
         h = __shfl_sync(FULL, h, 0);
-        const int g = lane >> 3;
+        const int g = lane / G1;
         int slot = -1;
-        if (g < k && (lane & 7) == 0) slot = wait_entry(e1.q, h + g);
-        slot = __shfl_sync(FULL, slot, lane & ~7);
+        if (g < k && (lane % G1) == 0) slot = wait_entry(e1.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~(G1 - 1));
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        if constexpr (PK) pk_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        if constexpr (PK) pk_resume<XDROP_T1_G, XDROP_T1_C>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
         else band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
         tl_rec(c, 3, t0);
         __threadfence();

@@ -5,7 +5,8 @@ os.environ["XDROP_TIMELINE"] = "1"
 import numpy as np
 import paper_2309_07270_b200 as xd
 from synth import workload as W
-w = W.config(sys.argv[1] if len(sys.argv) > 1 else "ecoli")
+_nm = sys.argv[1] if len(sys.argv) > 1 else "ecoli"
+w = W.config(_nm, scale=0.05) if _nm == "celegans" else W.config(_nm)
 with xd.Aligner() as al:
     for _ in range(2):
         r, c = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
