@@ -346,3 +346,21 @@ def test_packed_resume_reaches_s1024(xd):
     ref, rcells = oracle_of(w)
     assert_same(res, cells, ref, rcells, "packed resume S1024")
     assert st["escalated"][2] > 0, st["escalated"]
+
+
+def test_random_scoring_sweep_packed_and_32bit(xd):
+    """40 random (M, mu, g, X) settings across the API ranges, both sides of the packed-mode gate,
+    ragged strand-mixed batches: every field bit-exact against the oracle."""
+    from synth import workload as W
+    rng = np.random.default_rng(2024)
+    with xd.Aligner() as al:
+        for case in range(40):
+            M = int(rng.choice([1, 1, 2, 3, 5, 32]))
+            mu = -int(rng.choice([1, 1, 2, 4, 9, 64]))
+            g = -int(rng.choice([1, 1, 2, 3, 7, 64]))
+            X = int(rng.choice([0, 3, 15, 40, 200, 509 - M, 600]))
+            w = W.random_pairs_workload(seed=7000 + case, n_pairs=40, len_lo=0, len_hi=700, k=9, X=X,
+                                        rc_frac=0.3)
+            res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X, M=M, mu=mu, g=g)
+            ref, rcells = oracle_of(w, X=X, M=M, mu=mu, g=g)
+            assert_same(res, cells, ref, rcells, f"case {case}: M={M} mu={mu} g={g} X={X}")
