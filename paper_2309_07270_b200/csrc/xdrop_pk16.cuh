@@ -287,8 +287,11 @@ __device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo,
   B.best = up ? gv : B.best;
   B.istar = up ? ibase + tst : B.istar;
   B.jstar = up ? d - ibase - tst : B.jstar;
-  const int lo = max(max(0, d - B.n), min(B.minL1, B.minL2 + 1));
-  const int hi = min(min(B.m, d), max(B.maxL1, B.maxL2) + 1);
+  int lo = min(B.minL1, B.minL2 + 1), hi = max(B.maxL1, B.maxL2) + 1;
+  if constexpr (CHECK) {          // outside boundary blocks the live cells are off the matrix edges
+    lo = max(max(0, d - B.n), lo);
+    hi = min(min(B.m, d), hi);
+  }
   B.cells += max(0, hi - lo + 1);
   B.minL2 = B.minL1; B.maxL2 = B.maxL1;
   B.minL1 = mn; B.maxL1 = mx;
