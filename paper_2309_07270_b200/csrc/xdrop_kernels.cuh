@@ -650,8 +650,11 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 #include "xdrop_pk16.cuh"
 
 // Standalone kernel resuming checkpointed extensions in the packed 16-bit mode (X + M <= 510).
+#ifndef XDROP_PKR_MINBLOCKS
+#define XDROP_PKR_MINBLOCKS 3
+#endif
 template <int G, int C>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, XDROP_PKR_MINBLOCKS)
 pk_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   constexpr int IPW = 32 / G;
   const int lane = threadIdx.x & 31;
