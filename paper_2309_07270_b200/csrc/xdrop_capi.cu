@@ -264,17 +264,20 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     // T1 lane pair (S = 64), T2 warp (S = 256) in one persistent kernel; checkpoints of T2
     // resume in a warp with S = 1024; beyond that the unbounded kernel restarts the extension.
     int* items0 = D.items.as<int>();
-    const int64_t cap1 = std::min<int64_t>(n_items, 1 << 20), cap2 = std::min<int64_t>(n_items, 1 << 18),
-                  cap3 = std::min<int64_t>(n_items, 1 << 17);
-    const int64_t cap4 = std::min<int64_t>(n_items, 1 << 14);
-    // record sizes hold the source tier's window: T0 32, T1 64 (32-bit) / 128 (packed), T2 256, S1024
+    // checkpoint-record pools (never recycled within a call): every extension may escalate once per
+    // tier, so T1/T2 pools hold one record per item; the wide tiers are bounded by a byte budget
+    // (a full pool only sends the extension to the unbounded kernel, still exact)
+    const int64_t budget = (int64_t)4 << 30;
+    const int64_t cap1 = n_items, cap2 = n_items;
+    const int64_t cap3 = std::min<int64_t>(n_items, budget / ((xk::HDR + 2 * 256) * 4));
+    const int64_t cap4 = std::min<int64_t>(n_items, budget / 8 / ((xk::HDR + 2 * 1024) * 4));
     const int rec1 = xk::HDR + 2 * 32, rec2 = xk::HDR + 2 * 128, rec3 = xk::HDR + 2 * 256, rec4 = xk::HDR + 2 * 1024;
     CKR(D.pool1.ensure((size_t)std::max<int64_t>(cap1, 1) * rec1 * sizeof(int)));
     CKR(D.pool2.ensure((size_t)std::max<int64_t>(cap2, 1) * rec2 * sizeof(int)));
     CKR(D.pool3.ensure((size_t)std::max<int64_t>(cap3, 1) * rec3 * sizeof(int)));
     CKR(D.pool4.ensure((size_t)std::max<int64_t>(cap4, 1) * rec4 * sizeof(int)));
     CKR(D.q4.ensure((size_t)std::max<int64_t>(cap4, 1) * sizeof(int)));
-    const int64_t caps = std::min<int64_t>(n_items, 1 << 18);
+    const int64_t caps = n_items;                          // stolen lane-mode extensions (S = 32 records)
     CKR(D.pools.ensure((size_t)std::max<int64_t>(caps, 1) * rec1 * sizeof(int)));
     CKR(D.qs.ensure((size_t)std::max<int64_t>(caps, 1) * sizeof(int)));
     CK(cudaMemsetAsync(D.qs.p, 0xff, (size_t)std::max<int64_t>(caps, 1) * sizeof(int), s));
