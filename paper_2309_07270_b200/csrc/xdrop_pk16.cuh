@@ -94,12 +94,19 @@ template <int G, int C> struct Band16 {
   bool active;
 };
 
+// key bits of a cell: 31 - t with t the cell's index in the whole window when the window has at
+// most 32 cells (then the key maximum over the group is also the argmax), else its index in the
+// lane (wider groups break ties by lane with a ballot)
+template <int G, int C> __device__ __forceinline__ constexpr bool pk_global_keys() { return G * C <= 32; }
+template <int G, int C> __device__ __forceinline__ int pk_key_base(int gl) {
+  return pk_global_keys<G, C>() ? 31 - C * gl : 31;
+}
+
 // key bytes 31 - t; `zero` is an opaque 0 so the words stay in registers (PRMT operand c)
 template <int G, int C>
 __device__ __forceinline__ void pk_keys(Band16<G, C>& B, int gl, int zero) {
   constexpr int NP = C / 2;
-  const int tb = 31 + zero;                       // key bytes 31 - (local cell); G > 1 breaks ties by lane
-  (void)gl;
+  const int tb = pk_key_base<G, C>(gl) + zero;
 #pragma unroll
   for (int j = 0; j < NP / 2; ++j)
     B.TC[j] = opaque((uint32_t)(tb - 2 * j) | ((uint32_t)(tb - 2 * j - NP) << 8) |
@@ -258,6 +265,10 @@ __device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo,
   if constexpr (G == 1) {
     vrel = kl >> 5;
     tst = 31 - (kl & 31);
+  } else if constexpr (pk_global_keys<G, C>()) {         // window-wide keys: the max is the argmax
+    const int km = gmax<G>(kl);
+    vrel = km >> 5;
+    tst = 31 - (km & 31);
   } else {                                                // value first, then the lowest lane, then t
     const int vl = kl >> 5;
     vrel = gmax<G>(vl);
@@ -365,10 +376,10 @@ __device__ __forceinline__ void pk_shift1(uint32_t (&A)[NP], int gl, int dir) {
 // after a window shift: restore the key bits 31 - (local cell) of every pair (a shift moves lo
 // cells, whose keys reach 31, into hi halves, where the FMA-pipe adds may carry into the keys)
 template <int NP>
-__device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP]) {
+__device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP], int kb) {
 #pragma unroll
   for (int u = 0; u < NP; ++u)
-    A[u] = (A[u] & 0xFFE0FFE0u) | (uint32_t)(31 - u) | ((uint32_t)(31 - u - NP) << 16);
+    A[u] = (A[u] & 0xFFE0FFE0u) | (uint32_t)(kb - u) | ((uint32_t)(kb - u - NP) << 16);
 }
 
 // checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
@@ -454,7 +465,7 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
       sh = min(max(sh, -8), 8);
       if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
       pk_shift_n<C>(B, sh);
-      pk_rekey<C / 2>(B.E); pk_rekey<C / 2>(B.O);
+      pk_rekey<C / 2>(B.E, pk_key_base<G, C>(gl)); pk_rekey<C / 2>(B.O, pk_key_base<G, C>(gl));
       B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
       pk_reload<G, C>(B, gl, rem, P);
     }
@@ -470,7 +481,7 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
     }
     if (dir != 0) {
       pk_shift1<G, C / 2>(B.E, gl, dir); pk_shift1<G, C / 2>(B.O, gl, dir);
-      pk_rekey<C / 2>(B.E); pk_rekey<C / 2>(B.O);
+      pk_rekey<C / 2>(B.E, pk_key_base<G, C>(gl)); pk_rekey<C / 2>(B.O, pk_key_base<G, C>(gl));
       B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
       pk_reload<G, C>(B, gl, rem, P);
     }
@@ -562,7 +573,7 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
   {
     constexpr int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
     if (gl == (S / 2) / C) {
-      const uint32_t v0 = (uint32_t)(32 * P.X + 31 - tl) & 0xffffu;
+      const uint32_t v0 = (uint32_t)(32 * P.X + pk_key_base<G, C>(gl) - tl) & 0xffffu;
       B.E[u0] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
     }
   }
@@ -630,7 +641,7 @@ __device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int 
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int t = u + NP * h;
-      const uint32_t tc = 31 - t;
+      const uint32_t tc = pk_key_base<G, C>(gl) - t;
       const uint32_t ve = w_e[t] > 0 ? ((uint32_t)(32 * (w_e[t] - B.thrD)) | tc) & 0xffffu : 0xC000u | tc;
       const uint32_t vo = w_o[t] > 0 ? ((uint32_t)(32 * (w_o[t] - B.thrD1)) | tc) & 0xffffu : 0xC000u | tc;
       e |= ve << (16 * h); o |= vo << (16 * h);
