@@ -157,22 +157,27 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
                                              int gl, int qlo, int qhi, const Problem& P, uint32_t (&ch)[C > 16 ? 2 : 1]) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
   const int thr_d = B.thrN;
-  const int D1 = 32 * (B.thrD - thr_d);
-  const int Ev = 32 * (B.thrD1 - B.thrD);
-  const int sM = P.pkM + Ev, sU = P.pkU + Ev;            // s' + D2 - D1 for a match / a mismatch
-  const uint32_t base = __byte_perm((uint32_t)sM, 0u, 0x1010);
-  // sE = base + bits * kk, bits = (mismatch(lo), mismatch(hi) << 16); + 2^16 undoes the borrow
-  // of a negative lo half (the hi-half product drops it mod 2^32)
-  const uint32_t kk = (uint32_t)(sU - sM) + ((sU < 0 && sM >= 0) ? 0x10000u : 0u);
-  const uint32_t D1p = __byte_perm((uint32_t)D1, 0u, 0x1010);
+  const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
+  const uint32_t one = two >> 1;                          // 1, opaque: keeps the adds on IMAD
+  (void)one;
+  // per-anti-diagonal scalars on the FMA pipe (IMAD with opaque constants; the ALU pipe is the
+  // binding one): D1 = 32 (thrD - thr_d) < 0, Ev = 32 (thrD1 - thrD), s' + D2 - D1 = pk + Ev
+  const int k32 = (int)(two << 4), k65536 = (int)(two << 15), k65537 = k65536 + (int)one;
+  const int D1 = B.thrD * k32 - thr_d * k32;
+  const int Ev = B.thrD1 * k32 - B.thrD * k32;
+  const int sM = Ev * (int)one + P.pkM, sU = Ev * (int)one + P.pkU;   // match / mismatch
+  // packed pairs: (x, x) = x * 65537 (+ 2^16 when x < 0: the borrow of the low half)
+  const int negM = (int)__umulhi((uint32_t)sM, two), negU = (int)__umulhi((uint32_t)sU, two);
+  const uint32_t base = (uint32_t)(sM * k65537 + negM * k65536);
+  // sE = base + bits * kk, bits = (mismatch(lo), mismatch(hi) << 16); the 2^16 terms undo the
+  // borrows of negative low halves (the hi-half product drops them mod 2^32)
+  const uint32_t kk = (uint32_t)((negU - negM) * k65536 + (P.pkU - P.pkM));
+  const uint32_t D1p = (uint32_t)(D1 * k65537 + k65536);
   uint32_t mis = (B.A0 ^ B.B0) | (B.A1 ^ B.B1);           // bit tl: local cell tl compares unequal bases
   if constexpr (NP < 16) {                                // hi cells (tl >= NP) to bits 16..
     constexpr uint32_t LO = (1u << NP) - 1u;
     mis = (mis & LO) | ((mis << (16 - NP)) & (LO << 16));
   }
-  const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
-  const uint32_t one = two >> 1;                          // 1, opaque: keeps the adds on IMAD
-  (void)one;
   // seam pair: the neighbour cell beyond the lane's last (first) cell
   uint32_t seam;
   if constexpr (PAR == 0) {
