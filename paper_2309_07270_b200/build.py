@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libxdrop.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("xdrop_capi.cu", "sched.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("xdrop_kernels.cuh", "sched.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("xdrop_kernels.cuh", "xdrop_pk16.cuh", "sched.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "xdrop.h")]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared"]
