@@ -90,6 +90,11 @@ typedef struct {
 #define XDROP_FLAG_FORCE_WIDE 1    /* skip the lane-per-extension path (tests) */
 #define XDROP_FLAG_FORCE_GENERAL 2 /* send every extension to the unbounded fallback (tests) */
 #define XDROP_FLAG_NO_SORT 4       /* do not length-sort the work queue (tests) */
+/* Packed-mode band kernel (X + M <= 510).  Default: chosen per call from the previous
+ * call's escalation count on the device (the shared kernel once escalated work alone can fill the
+ * GPU's resident warps, else the tiered one); results are identical either way. */
+#define XDROP_FLAG_TIERED 8        /* always the tiered kernel (small per-tier loops, short tails) */
+#define XDROP_FLAG_SHARED 16       /* always the shared kernel (one loop for every tier, no I$ thrash) */
 
 /* A read pool in HOST memory: ASCII bases, read r = seq[offsets[r] .. offsets[r+1]). */
 typedef struct {
@@ -169,6 +174,7 @@ typedef struct {
   int64_t level_items[4]; /* extensions completed at each level */
   int64_t long_items;     /* extensions run in the multi-lane "long" mode of level 0 */
   int64_t stolen;         /* lane-mode extensions checkpointed at the tail and resumed 4 lanes wide */
+  int64_t band_kernel;    /* band kernel of the call: 0 32-bit merged, 1 packed tiered, 2 packed shared */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 

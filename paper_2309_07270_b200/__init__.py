@@ -144,7 +144,8 @@ class Aligner:
         return dict(items=s.items, escalated=list(s.escalated), kernel_ms=s.kernel_ms, total_ms=s.total_ms,
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
                     level_cells=list(s.level_cells), level_items=list(s.level_items),
-                    long_items=s.long_items, stolen=s.stolen)
+                    long_items=s.long_items, stolen=s.stolen,
+                    band_kernel=("merged32", "tiered", "shared")[s.band_kernel])
 
     def sched_stats(self) -> dict:
         s = N.SchedStats()

@@ -90,13 +90,17 @@ struct DevCtx {
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
+  int64_t last_t1 = 0;      // T0 -> T1 checkpoints of the previous packed call (kernel choice)
+  int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per call
+  int age_us = 20;           // T1/T2 batch claims go partial once the oldest record waited this long (XDROP_AGE_US)
   int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
   int t0_per_sm = 3;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
   bool pk16 = true;          // packed 16-bit lane mode for T0 (XDROP_PK16=0: 32-bit lane mode)
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf;
+  xk::PkTier tier_host[3];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -131,14 +135,14 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
   if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
   if (D.long_g == 2) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16, false>, 128, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 2, 16, true>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<2, 16>, 128, 0));
   } else if (D.long_g == 4) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8, false>, 128, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 4, 8, true>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<4, 8>, 128, 0));
   } else {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32, false>, 128, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::band_merged_kernel<32, 1, 32, true>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<4, 8>, 128, 0));
   }
   D.occ_pk = std::max(1, D.occ_pk);
   // resident blocks per SM of the packed merged kernel: fewer co-resident warps shorten the
@@ -148,6 +152,8 @@ int dev_open(DevCtx& D, int dev) {
     if (const char* e = getenv("XDROP_OCC")) D.occ_pk = std::max(1, std::min(occ_max, atoi(e)));
     if (const char* e = getenv("XDROP_T0_PER_SM")) D.t0_per_sm = std::max(0, atoi(e));
     if (const char* e = getenv("XDROP_IDLE_NS")) D.idle_ns = std::max(0, atoi(e));
+    if (const char* e = getenv("XDROP_AGE_US")) D.age_us = std::max(0, atoi(e));
+    if (const char* e = getenv("XDROP_KERNEL")) D.kernel_env = atoi(e);
     if (D.t0_per_sm <= 0) D.t0_per_sm = D.occ_pk;
   }
   CKR(D.smcnt.ensure(1024 * sizeof(int)));
@@ -170,7 +176,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -194,7 +200,7 @@ int pack_pool(DevCtx& D, const char* d_seq, int64_t len, Buf& out, cudaStream_t 
   return cuda_err(cudaGetLastError());
 }
 
-struct Flags { bool force_wide, force_general, nosort; };
+struct Flags { bool force_wide, force_general, nosort, tiered, shared; };
 
 // The device pipeline on one GPU.  All pointers are device pointers.
 // out5 / cells may be the caller's buffers (device API) or D's workspaces.
@@ -299,7 +305,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
                        ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
                        (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * t0b * 4 * 32), 1 << 30),
-                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns};
+                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns, D.age_us};
       CK(cudaMemsetAsync(D.smcnt.p, 0, 1024 * sizeof(int), s));
       if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
         CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
@@ -312,18 +318,38 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
       const unsigned grid = (unsigned)(D.sms * occ);
-      if (D.long_g == 2 && pk)
-        xk::band_merged_kernel<32, 2, 16, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (D.long_g == 2)
-        xk::band_merged_kernel<32, 2, 16, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (D.long_g == 4 && pk)
-        xk::band_merged_kernel<32, 4, 8, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (D.long_g == 4)
-        xk::band_merged_kernel<32, 4, 8, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      // the packed kernel reads its tier descriptors from device memory where used (rare paths)
+      const xk::PkTier* tiers = nullptr;
+      if (pk) {
+        CKR(D.escbuf.ensure(3 * sizeof(xk::PkTier)));
+        D.tier_host[0] = xk::PkTier{e1, e1, nullptr, nullptr, 0};                   // fresh (T0)
+        D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
+        D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, nullptr, 1};               // T2 pool
+        CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 3 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
+        tiers = D.escbuf.as<xk::PkTier>();
+      }
+      // packed kernel per call: the shared one when the previous call's escalated
+      // extensions alone could fill every resident T1 group twice over, else the tiered one
+      int shared = 0;
+      if (pk) {
+        const int64_t groups = (int64_t)D.sms * occ * 4 * (32 / XDROP_T1_G);
+        shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2) : (D.last_t1 >= 2 * groups);
+      }
+      D.st.band_kernel = pk ? 1 + shared : 0;
+      if (pk && shared && D.long_g == 2)
+        xk::pk_merged_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+      else if (pk && shared)      // long_g 4, or 1 (no long mode: n_long = 0)
+        xk::pk_merged_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+      else if (pk && D.long_g == 2)
+        xk::pk_tiered_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (pk)
-        xk::band_merged_kernel<32, 1, 32, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::pk_tiered_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (D.long_g == 2)
+        xk::band_merged_kernel<32, 2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (D.long_g == 4)
+        xk::band_merged_kernel<32, 4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else
-        xk::band_merged_kernel<32, 1, 32, false><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+        xk::band_merged_kernel<32, 1, 32><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
@@ -354,6 +380,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
     D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_P1];
     D.st.escalated[1] = hs[C_P2];
+    if (pk && !fl.force_wide && !fl.force_general) D.last_t1 = hs[C_P1];
     D.st.escalated[2] = hs[C_P3];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
@@ -498,6 +525,8 @@ static Flags flags_of(const xdrop_ctx* ctx) {
   f.force_wide = (ctx->opts.flags & XDROP_FLAG_FORCE_WIDE) != 0;
   f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0;
   f.nosort = (ctx->opts.flags & XDROP_FLAG_NO_SORT) != 0;
+  f.tiered = (ctx->opts.flags & XDROP_FLAG_TIERED) != 0;
+  f.shared = (ctx->opts.flags & XDROP_FLAG_SHARED) != 0;
   return f;
 }
 

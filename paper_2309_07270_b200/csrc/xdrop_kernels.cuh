@@ -381,6 +381,12 @@ struct Esc {
   int* fb_tail;
 };
 constexpr int HDR = 32;
+constexpr int REC_T = 17;          // header int: publication time (globaltimer >> 10, ~us) of the record
+__device__ __forceinline__ int rec_stamp() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return (int)(unsigned)(t >> 10);
+}
 
 // queue push: slot = atomicAdd(tail); store; fence (consumers may be running)
 __device__ __forceinline__ void push_item(int* items, int* tail, int item) {
@@ -406,6 +412,7 @@ __device__ __forceinline__ void band_save(const Band<C>& B, int gl, int d, const
     rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
     rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = S;
     rec[15] = (int)(B.cells & 0xffffffffll); rec[16] = (int)(B.cells >> 32);
+    rec[REC_T] = rec_stamp();
   }
 #pragma unroll
   for (int r = 0; r < 2 * C; ++r) rec[HDR + 2 * C * gl + r] = B.R[r];
@@ -647,6 +654,47 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   }
 }
 
+// claim up to `want` published entries of a queue (lane 0 only); returns the
+// first claimed index and sets k (0: nothing claimed)
+__device__ __forceinline__ int claim(int* head, const int* tail, int want, bool partial, int& k) {
+  k = 0;
+  int h = ld_volatile(head);
+  for (;;) {
+    const int t = ld_volatile(tail);
+    const int avail = t - h;
+    if (avail <= 0 || (avail < want && !partial)) return 0;
+    const int kk = min(want, avail);
+    const int old = atomicCAS(head, h, h + kk);
+    if (old == h) { k = kk; return h; }
+    h = old;
+  }
+}
+// claim for a batch consumer: up to `want` entries, fewer only when `partial` or the oldest unclaimed
+// record has waited >= age_us (lane 0 only)
+__device__ __forceinline__ int claim_batch(int* head, const Esc& e, int want, bool partial, int age_us, int& k) {
+  k = 0;
+  const int h = ld_volatile(head), t = ld_volatile(e.q_tail);
+  if (t <= h) return 0;
+  if (!partial && t - h < want) {
+    const int slot = ld_volatile(e.q + h);
+    if (slot < 0) return 0;
+    const int st = ld_volatile(e.pool + (size_t)slot * e.rec_ints + REC_T);
+    if ((int)((unsigned)rec_stamp() - (unsigned)st) < age_us) return 0;
+  }
+  return claim(head, e.q_tail, want, true, k);
+}
+__device__ __forceinline__ int wait_entry(const int* q, int i) {
+  int v;
+  do { v = ld_volatile(q + i); } while (v < 0);
+  return v;
+}
+// the one claimed entry h of a warp-wide consumer (lane 0 waits, all lanes get it)
+__device__ __forceinline__ int wait_entry_w(const int* q, int h, int lane) {
+  int slot = -1;
+  if (lane == 0) slot = wait_entry(q, h);
+  return __shfl_sync(FULL, slot, 0);
+}
+
 #include "xdrop_pk16.cuh"
 
 // Standalone kernel resuming checkpointed extensions in the packed 16-bit mode (X + M <= 510).
@@ -676,7 +724,8 @@ struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_
                    int* idle; int* qs_head; int* dones;
                    unsigned long long* tl; int* tl_n; int tl_cap;     // optional work-unit timeline
                    int endgame;                                       // T0 items left -> 4-lane dispatch
-                   int* smcnt; int t0_per_sm; int idle_ns; };                      // blocks per SM that take T0 work
+                   int* smcnt; int t0_per_sm; int idle_ns;
+                   int age_us; };                     // batch claims of T1/T2 go partial after this wait                      // blocks per SM that take T0 work
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -692,72 +741,35 @@ __device__ __forceinline__ void tl_rec(const MergedCtr& c, int type, unsigned lo
   c.tl[3 * i] = (unsigned long long)type | (w << 8); c.tl[3 * i + 1] = t0; c.tl[3 * i + 2] = gtimer();
 }
 
-// claim up to `want` published entries of a queue (lane 0 only); returns the
-// first claimed index and sets k (0: nothing claimed)
-__device__ __forceinline__ int claim(int* head, const int* tail, int want, bool partial, int& k) {
-  k = 0;
-  int h = ld_volatile(head);
-  for (;;) {
-    const int t = ld_volatile(tail);
-    const int avail = t - h;
-    if (avail <= 0 || (avail < want && !partial)) return 0;
-    const int kk = min(want, avail);
-    const int old = atomicCAS(head, h, h + kk);
-    if (old == h) { k = kk; return h; }
-    h = old;
-  }
-}
-__device__ __forceinline__ int wait_entry(const int* q, int i) {
-  int v;
-  do { v = ld_volatile(q + i); } while (v < 0);
-  return v;
-}
-
-// Tiers 0-2 in ONE persistent kernel.
+// Tiers 0-2 in ONE persistent kernel (32-bit cells; the packed mode is pk_merged_kernel below).
 //  T0  fresh extensions: the longest (the first n_long of the length-sorted
 //      queue; n_long is set on the device from the batch's total work per
 //      resident lane, see scan_kernel) run GL lanes per extension (CL cells,
 //      same 32-cell window) so their anti-diagonal chain -- the launch's
 //      critical path -- is GL times shorter per step; the rest run one lane
 //      per extension (C0 = 32 cells).
-//  T1  checkpointed T0 extensions resume two lanes per extension (S = 64),
-//      16 per warp, as soon as 16 are queued (or T0 has no work left).
+//  T1  checkpointed T0 extensions resume 8 lanes x 8 cells per extension (S = 64),
+//      claimed as soon as they appear.
 //  T2  checkpointed T1 extensions resume one warp per extension (S = 256).
 //  T2 overflows are checkpointed for the separate S = 1024 launch.
 // Escalated work takes priority, so it runs while T0 drains, not as a tail.
 #ifndef XDROP_MERGED_MINBLOCKS
 #define XDROP_MERGED_MINBLOCKS 3
 #endif
-// packed T1 / T2 shapes.  Measured (E. coli, C. elegans x0.05, X-sweep): the escalation tiers are
-// latency-bound (their extensions escalated late and run alone), so few cells per lane win:
-// T1 8 x 8 (S = 64) and T2 32 x 8 (S = 256, one per warp) beat 8 x 16 / 16 x 8 (S = 128) and
-// 16 x 16 (two per warp) everywhere except X = 100
+// packed escalation tiers (pk_merged_kernel): T1 = XDROP_T1_G lanes x 32 cells, T2 = XDROP_T2_G x 32
 #ifndef XDROP_T1_G
-#define XDROP_T1_G 8
-#endif
-#ifndef XDROP_T1_C
-#define XDROP_T1_C 8
+#define XDROP_T1_G 4
 #endif
 #ifndef XDROP_T2_G
-#define XDROP_T2_G 32
-#endif
-#ifndef XDROP_PK_C
-#define XDROP_PK_C 32          // cells per lane of the packed lane mode
+#define XDROP_T2_G 8
 #endif
 #ifndef XDROP_PK_MINBLOCKS
 #define XDROP_PK_MINBLOCKS 3
 #endif
-template <int C0, int GL, int CL, bool PK>
-__global__ void __launch_bounds__(128, PK ? XDROP_PK_MINBLOCKS : XDROP_MERGED_MINBLOCKS)
-band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
-                   Esc e1, Esc e2, Esc e3, Steal st) {
-  const int lane = threadIdx.x & 31;
-  const int n_items = *n_items_ptr;
-  const int n_long = min(*c.n_long, n_items);
-  const int first = (GL > 1) ? n_long : 0;
-  // the first t0_per_sm resident blocks of each SM take fresh (T0) extensions; the others serve
-  // only escalated / stolen work, so T0's lane warps keep their issue share (the longest
-  // extensions' anti-diagonal chains set the launch's tail) while wide bands still find warps
+
+// the first t0_per_sm resident blocks of each SM take fresh (T0) extensions; the others serve
+// only escalated / stolen work
+__device__ __forceinline__ bool t0_block(const MergedCtr& c) {
   __shared__ int s_t0;
   if (threadIdx.x == 0) {
     unsigned smid;
@@ -765,50 +777,63 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
     s_t0 = (c.t0_per_sm <= 0) || atomicAdd(c.smcnt + (smid & 1023), 1) < c.t0_per_sm;
   }
   __syncthreads();
-  const bool t0ok = s_t0 != 0;
+  return s_t0 != 0;
+}
+
+// no work visible: finished once T0 is done (=> T1's queue is final), T1 is done (=> T2's queue is
+// final) and T2's queue is drained (stolen records come only from T0 batches, before their done0 add)
+__device__ __forceinline__ bool merged_finished(const MergedCtr& c, int n_items, const Esc& e1, const Esc& e2,
+                                                const Steal& st) {
+  if (ld_volatile(c.done0) < n_items) return false;
+  const int ts = ld_volatile(st.es.q_tail);
+  if (ld_volatile(c.dones) < ts || ld_volatile(c.qs_head) < ts) return false;
+  const int t1 = ld_volatile(e1.q_tail);
+  if (ld_volatile(c.done1) < t1 || ld_volatile(c.q1_head) < t1) return false;
+  return ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
+}
+
+template <int C0, int GL, int CL>
+__global__ void __launch_bounds__(128, XDROP_MERGED_MINBLOCKS)
+band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
+                   Esc e1, Esc e2, Esc e3, Steal st) {
+  const int lane = threadIdx.x & 31;
+  const int n_items = *n_items_ptr;
+  const int n_long = min(*c.n_long, n_items);
+  const int first = (GL > 1) ? n_long : 0;
+  const bool t0ok = t0_block(c);
   bool idle = false;                    // this warp is counted in *c.idle
   unsigned nap = 1000;                  // current poll period of an escalation-only warp (ns)
   auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; nap = 1000; };
   for (;;) {
-    // T2 (S = 256): 32 / XDROP_T2_G extensions per warp (packed), one per warp (32-bit)
+    // T2 (S = 256): one extension per warp
     {
-      constexpr int W2 = PK ? 32 / XDROP_T2_G : 1;
       int k = 0, h = 0;
-      if (lane == 0) h = claim(c.q2_head, e2.q_tail, W2, true, k);
+      if (lane == 0) h = claim(c.q2_head, e2.q_tail, 1, true, k);
       k = __shfl_sync(FULL, k, 0);
       if (k) {
         h = __shfl_sync(FULL, h, 0);
-        const int g = lane / (32 / W2);
-        int slot = -1;
-        if (g < k && (lane % (32 / W2)) == 0) slot = wait_entry(e2.q, h + g);
-        slot = __shfl_sync(FULL, slot, lane & ~(32 / W2 - 1));
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        const int* rec = slot >= 0 ? e2.pool + (size_t)slot * e2.rec_ints : nullptr;
-        if constexpr (PK) pk_resume<XDROP_T2_G, 256 / XDROP_T2_G>(P, rec, 1, e3);
-        else band_resume<32, 8>(P, rec, 1, e3);
+        const int slot = wait_entry_w(e2.q, h, lane);
+        band_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
         tl_rec(c, 4, t0);
         continue;
       }
     }
-    // T1: up to 4 checkpointed extensions per warp, eight lanes x 8 cells (S = 64),
-    // claimed as soon as they appear: few extensions get here and each one escalated late in
-    // its life, so a short per-anti-diagonal latency matters more than full lanes
+    // T1: up to 4 checkpointed extensions per warp, eight lanes x 8 cells (S = 64)
     {
-      constexpr int G1 = PK ? XDROP_T1_G : 8, W1 = 32 / G1;
       int k = 0, h = 0;
-      if (lane == 0) h = claim(c.q1_head, e1.q_tail, W1, true, k);
+      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 4, true, k);
       k = __shfl_sync(FULL, k, 0);
       if (k) {
         h = __shfl_sync(FULL, h, 0);
-        const int g = lane / G1;
+        const int g = lane >> 3;
         int slot = -1;
-        if (g < k && (lane % G1) == 0) slot = wait_entry(e1.q, h + g);
-        slot = __shfl_sync(FULL, slot, lane & ~(G1 - 1));
+        if (g < k && (lane & 7) == 0) slot = wait_entry(e1.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~7);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        if constexpr (PK) pk_resume<XDROP_T1_G, XDROP_T1_C>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
-        else band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        band_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
         tl_rec(c, 3, t0);
         __threadfence();
         __syncwarp();
@@ -829,8 +854,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         slot = __shfl_sync(FULL, slot, lane & ~3);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        if constexpr (PK) pk_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
-        else band_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        band_resume<4, 8>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
         tl_rec(c, 2, t0);
         __threadfence();
         __syncwarp();
@@ -847,8 +871,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
         const int slot = base + lane / GL;
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        if constexpr (PK) pk_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
-        else band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        band_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
         tl_rec(c, 1, t0);
         __threadfence();
         __syncwarp();
@@ -873,8 +896,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       const unsigned long long t0 = c.tl ? gtimer() : 0;
       if (take == 32) {
         const int slot = base + lane;
-        if constexpr (PK) pk_run<1, XDROP_PK_C>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
-        else band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+        band_run<1, C0>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
         tl_rec(c, 0, t0);
       } else {
         const int slot = base + (lane >> 2);
@@ -886,25 +908,233 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
       if (lane == 0) atomicAdd(c.done0, min(take, n_items - base));
       continue;
     }
-    // no work visible: finished once T0 is done (=> T1's queue is final), T1 is
-    // done (=> T2's queue is final) and T2's queue is drained
-    // (stolen records come only from T0 batches, before their done0 add)
     int fin = 0;
     if (lane == 0) {
-      if (ld_volatile(c.done0) >= n_items) {
-        const int ts = ld_volatile(st.es.q_tail);
-        if (ld_volatile(c.dones) >= ts && ld_volatile(c.qs_head) >= ts) {
-          const int t1 = ld_volatile(e1.q_tail);
-          if (ld_volatile(c.done1) >= t1 && ld_volatile(c.q1_head) >= t1)
-            fin = ld_volatile(c.q2_head) >= ld_volatile(e2.q_tail);
-        }
-      }
+      fin = merged_finished(c, n_items, e1, e2, st);
       if (!fin && !idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
     }
     fin = __shfl_sync(FULL, fin, 0);
     if (fin) break;
     // escalation-only warps back off exponentially while their queues stay empty (their polling
     // of the hot queue counters otherwise slows the T0 warps measurably)
+    __nanosleep(t0ok ? 1000 : nap);
+    if (!t0ok) nap = min(2 * nap, c.idle_ns);
+  }
+}
+
+// The packed-mode merged kernel (X + M <= 510): the same tiers and queues as band_merged_kernel,
+// with two loop instances, each at one call site, so the hot code stays in the instruction cache
+// (a loop per tier did not fit: DESIGN.md §7):
+//   pk_unit<32> with a run-time G: T0 lane mode G = 1 (S = 32, 32 fresh extensions per warp),
+//                 T1 G = XDROP_T1_G (S = 128) and T2 G = XDROP_T2_G (S = 256), 32/G extensions
+//                 per warp, refilling
+//   long T0 extensions from their seed and stolen lane-mode extensions: one GL x CL instance.  T1/T2 wait for a full batch of records
+// unless the oldest queued one has waited age_us or T0 has been fully claimed.
+template <int GL, int CL>
+__global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
+pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
+                 const PkTier* tiers, Steal st) {
+  static_assert(GL * CL == 32, "4-lane units keep the lane window");
+  enum { NONE = 0, FRESH, T1, T2, STOLEN, LONG };
+  const int lane = threadIdx.x & 31;
+  const int n_items = *n_items_ptr;
+  const int n_long = min(*c.n_long, n_items);
+  const int first = n_long;
+  const bool t0ok = t0_block(c);
+  bool idle = false;
+  unsigned nap = 1000;
+  for (;;) {
+    // lane 0 picks the unit: T2, T1, stolen, long, fresh (escalated work first)
+    int kind = NONE, h = 0, k = 0, base = 0;
+    if (lane == 0) {
+      const bool t0_over = ld_volatile(c.head0) + first >= n_items;
+      h = claim_batch(c.q2_head, tiers[2].src, 32 / XDROP_T2_G, t0_over, c.age_us, k);
+      if (k) kind = T2;
+      if (!kind) { h = claim_batch(c.q1_head, tiers[1].src, 32 / XDROP_T1_G, t0_over, c.age_us, k); if (k) kind = T1; }
+      if (!kind) { h = claim(c.qs_head, st.es.q_tail, 32 / GL, true, k); if (k) kind = STOLEN; }
+      if (!kind && t0ok && ld_volatile(c.head_long) < n_long) {
+        base = atomicAdd(c.head_long, 32 / GL);
+        if (base < n_long) kind = LONG;
+      }
+      if (!kind && t0ok && !t0_over) {
+        base = first + atomicAdd(c.head0, 32);
+        if (base < n_items) kind = FRESH;
+      }
+      if (kind && idle) { atomicSub(c.idle, 1); idle = false; }
+      if (!kind) {
+        if (merged_finished(c, n_items, tiers[1].src, tiers[2].src, st)) kind = -1;
+        else if (!idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
+      } else {
+        nap = 1000;
+      }
+    }
+    kind = __shfl_sync(FULL, kind, 0);
+    if (kind < 0) break;
+    if (kind == NONE) {
+      // escalation-only warps back off exponentially while their queues stay empty
+      __nanosleep(t0ok ? 1000 : nap);
+      if (!t0ok) nap = min(2 * nap, c.idle_ns);
+      continue;
+    }
+    h = __shfl_sync(FULL, h, 0);
+    k = __shfl_sync(FULL, k, 0);
+    base = __shfl_sync(FULL, base, 0);
+    const unsigned long long t0 = c.tl ? gtimer() : 0;
+    if (kind == STOLEN || kind == LONG) {
+      // one GL x CL instance for both: fresh from the seed (long) or from a stolen record
+      const int g = lane / GL, gl = lane % GL;
+      Band16<CL> B;
+      int d = 0;
+      pk_keys<CL>(B, GL, gl, P.keym >> 8);
+      if (kind == LONG) {
+        const int slot = base + g;
+        pk_init_seed<CL>(B, GL, gl, slot < n_long ? items[slot] : -1, P);
+      } else {
+        int slot = -1;
+        if (g < k && gl == 0) slot = wait_entry(st.es.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~(GL - 1));
+        pk_resume_init<CL>(B, GL, gl, d, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, P);
+      }
+      pk_loop<CL>(B, GL, gl, d, P, 0, tiers[0].esc, nullptr);
+      tl_rec(c, kind == LONG ? 1 : 2, t0);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        if (kind == LONG) atomicAdd(c.done0, min(32 / GL, n_long - base));
+        else atomicAdd(c.dones, k);
+      }
+    } else {
+      // T0 lane mode (G = 1), T1 (G = XDROP_T1_G) and T2 (G = XDROP_T2_G): one loop instance
+      const int t = kind == FRESH ? 0 : kind == T1 ? 1 : 2;
+      pk_unit<32>(P, t == 0 ? 1 : t == 1 ? XDROP_T1_G : XDROP_T2_G, t, tiers, items, base, n_items, h, k, st);
+      tl_rec(c, t == 0 ? 0 : t == 1 ? 3 : 4, t0);
+      if (t == 0) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
+      }
+    }
+  }
+}
+
+// The packed-mode TIERED kernel: a compile-time loop instance per tier with few cells per lane in
+// the escalation tiers (T1 = 8 lanes x 8 cells, S = 64, claimed as soon as records appear;
+// T2 = 32 lanes x 8 cells, S = 256, one per warp; 4-lane units for long / stolen extensions).
+// Short anti-diagonal latency for the escalated extensions, so they never become the launch's
+// tail; but with several hot loops on an SM it stalls on instruction fetch once escalated work
+// is a large share of the batch.  xdrop_capi.cu picks it or pk_merged_kernel per call (§7).
+template <int GL, int CL>
+__global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
+pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
+                 Esc e1, Esc e2, Esc e3, Steal st) {
+  const int lane = threadIdx.x & 31;
+  const int n_items = *n_items_ptr;
+  const int n_long = min(*c.n_long, n_items);
+  const int first = n_long;
+  const bool t0ok = t0_block(c);
+  bool idle = false;
+  unsigned nap = 1000;
+  auto busy = [&]() { if (idle && lane == 0) atomicSub(c.idle, 1); idle = false; nap = 1000; };
+  for (;;) {
+    // T2 (S = 256): one extension per warp, 32 lanes x 8 cells
+    {
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.q2_head, e2.q_tail, 1, true, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        const int slot = wait_entry_w(e2.q, h, lane);
+        pk_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        tl_rec(c, 4, t0);
+        continue;
+      }
+    }
+    // T1: up to 4 checkpointed extensions per warp, 8 lanes x 8 cells (S = 64)
+    {
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.q1_head, e1.q_tail, 4, true, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        const int g = lane >> 3;
+        int slot = -1;
+        if (g < k && (lane & 7) == 0) slot = wait_entry(e1.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~7);
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        pk_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        tl_rec(c, 3, t0);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.done1, k);
+        continue;
+      }
+    }
+    // stolen lane-mode extensions: 32/GL per warp, GL lanes each (same 32-cell window)
+    {
+      int k = 0, h = 0;
+      if (lane == 0) h = claim(c.qs_head, st.es.q_tail, 32 / GL, true, k);
+      k = __shfl_sync(FULL, k, 0);
+      if (k) {
+        h = __shfl_sync(FULL, h, 0);
+        const int g = lane / GL;
+        int slot = -1;
+        if (g < k && (lane % GL) == 0) slot = wait_entry(st.es.q, h + g);
+        slot = __shfl_sync(FULL, slot, lane & ~(GL - 1));
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        pk_resume<GL, CL>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        tl_rec(c, 2, t0);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.dones, k);
+        continue;
+      }
+    }
+    // T0: long extensions, 32/GL per warp
+    if (t0ok) {
+      int base = n_long;
+      if (lane == 0 && ld_volatile(c.head_long) < n_long) base = atomicAdd(c.head_long, 32 / GL);
+      base = __shfl_sync(FULL, base, 0);
+      if (base < n_long) {
+        const int slot = base + lane / GL;
+        busy();
+        const unsigned long long t0 = c.tl ? gtimer() : 0;
+        pk_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        tl_rec(c, 1, t0);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(c.done0, min(32 / GL, n_long - base));
+        continue;
+      }
+    }
+    // T0: the rest, 32 per warp (lane per extension)
+    int base = n_items;
+    if (lane == 0 && t0ok) {
+      const int h0 = first + ld_volatile(c.head0);
+      if (h0 < n_items) base = first + atomicAdd(c.head0, 32);
+    }
+    base = __shfl_sync(FULL, base, 0);
+    if (base < n_items) {
+      busy();
+      const unsigned long long t0 = c.tl ? gtimer() : 0;
+      const int slot = base + lane;
+      pk_run<1, 32>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+      tl_rec(c, 0, t0);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(c.done0, min(32, n_items - base));
+      continue;
+    }
+    int fin = 0;
+    if (lane == 0) {
+      fin = merged_finished(c, n_items, e1, e2, st);
+      if (!fin && !idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
+    }
+    fin = __shfl_sync(FULL, fin, 0);
+    if (fin) break;
     __nanosleep(t0ok ? 1000 : nap);
     if (!t0ok) nap = min(2 * nap, c.idle_ns);
   }

@@ -1,19 +1,25 @@
-// xdrop_pk16.cuh -- packed 16-bit band mode of tier T0 (included by xdrop_kernels.cuh).
+// xdrop_pk16.cuh -- packed 16-bit band mode (included by xdrop_kernels.cuh).
 //
-// Same operation as band_run<G, 32/G> (G lanes per extension, a window of 32
-// cells per anti-diagonal = 64 diagonals, exact checkpoints to the 32-bit
-// tiers), but the cells of an anti-diagonal are held as PAIRS of 16-bit values
-// and updated with the sm_100a dynamic-programming instructions
-// (VIMNMX.S16x2 / VIADDMNMX.S16x2), two cells per instruction.  G = 1 is the
-// lane-per-extension mode; G = 2 / 4 shorten the anti-diagonal chain of the
-// longest extensions (the launch's critical path).
+// Same operation as band_run<G, C> (G lanes per extension, a window of S = G*C
+// cells per anti-diagonal = 2S diagonals, exact checkpoints to the 32-bit
+// record format), but the cells of an anti-diagonal are held as PAIRS of 16-bit
+// values and updated with the sm_100a dynamic-programming instructions
+// (VIMNMX.S16x2 / VIADDMNMX.S16x2), two cells per instruction.
 //
-// Layout.  Cell t (0..31) of parity p sits on diagonal K0 + 2t + p; lane gl of
-// a group owns cells t = gl*C + tl, tl < C = 32/G.  Pair u of a parity array
-// holds local cells (u, u + NP), NP = C/2 -- lo and hi half.  With this strided
-// pairing the two neighbours of every pair are again whole pairs (for even
-// cells: odd pairs u-1 and u; for odd cells: even pairs u and u+1); only the
-// pair at the seam needs one PRMT (and one shuffle from the next lane).
+// G is a plain function argument (every function is force-inlined): a constant
+// G folds to the specialised code (pk_tiered_kernel: one instance per tier), and
+// pk_merged_kernel ("shared") runs ONE instance of the C = 32 loop with a
+// run-time G for the lane tier (G = 1, S = 32) and the escalation tiers
+// (G = 4, S = 128; G = 8, S = 256).  One hot loop instead of one per tier keeps
+// the kernel's hot code inside the SM's instruction cache (with a
+// loop per tier the C. elegans-shaped batch stalled on instruction fetch).
+//
+// Layout.  Cell t of parity p sits on diagonal K0 + 2t + p; lane gl of a group
+// owns cells t = gl*C + tl, tl < C.  Pair u of a parity array holds local cells
+// (u, u + NP), NP = C/2 -- lo and hi half.  With this strided pairing the two
+// neighbours of every pair are again whole pairs (for even cells: odd pairs u-1
+// and u; for odd cells: even pairs u and u+1); only the pair at the seam needs
+// one PRMT (and one shuffle from the next lane).
 //
 // Values.  A cell of anti-diagonal d is stored RELATIVE to the pruning
 // threshold of d and scaled by 32:  v = 32 * (W - thrW_d) + (31 - t), W the
@@ -27,11 +33,11 @@
 // Dead cells are forced to 0xC0xx (below any value a live predecessor can
 // give) by one PRMT (sign of each half replicated into a byte mask, with the
 // 31 - t key bytes inserted) and one LOP3.  The PRMT masks of 8 pairs are also
-// accumulated by one IMAD each into a word from which the 32 dead bits of the
+// accumulated by one IMAD each into a word from which the dead bits of the
 // anti-diagonal are decoded exactly (live extent, hull count).
 //
 // Range: live values are < 32 (X + M) + 32, so this mode requires X + M <= 510
-// (xdrop_capi.cu falls back to the 32-bit lane mode otherwise).
+// (xdrop_capi.cu falls back to the 32-bit kernels otherwise).
 #pragma once
 
 #ifndef XDROP_PK_FMA
@@ -76,7 +82,31 @@ __device__ __forceinline__ uint32_t plane32(uint64_t w, int b) {
   return even_bits16((uint32_t)(w >> b)) | (even_bits16((uint32_t)(w >> 32 >> b)) << 16);
 }
 
-template <int G, int C> struct Band16 {
+// lanes of this lane's group of G (G a power of two <= 32)
+__device__ __forceinline__ unsigned gmask(int G) {
+  if (G == 32) return FULL;
+  const int lane = threadIdx.x & 31;
+  return ((1u << G) - 1u) << (lane & ~(G - 1));
+}
+// max / min over the lanes of each group of G (all 32 lanes converged; xor partners stay in the group)
+__device__ __forceinline__ int gmax_rt(int v, int G) {
+  if (G == 32) return __reduce_max_sync(FULL, v);
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ int gmin_rt(int v, int G) {
+  if (G == 32) return __reduce_min_sync(FULL, v);
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+// min over this group's lanes only (callable from group-divergent code)
+__device__ __forceinline__ int gmin_grp(int v, int G) {
+  const unsigned gm = gmask(G);
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(gm, v, o));
+  return v;
+}
+
+template <int C> struct Band16 {
   static constexpr int NP = C / 2;
   uint32_t E[NP], O[NP];          // even / odd cells, pair u = (local cell u, local cell u + NP)
   uint32_t TC[NP / 2];            // key bytes 31 - t of pairs 2j, 2j+1: [lo(2j), hi(2j), lo(2j+1), hi(2j+1)]
@@ -96,17 +126,15 @@ template <int G, int C> struct Band16 {
 
 // key bits of a cell: 31 - t with t the cell's index in the whole window when the window has at
 // most 32 cells (then the key maximum over the group is also the argmax), else its index in the
-// lane (wider groups break ties by lane with a ballot)
-template <int G, int C> __device__ __forceinline__ constexpr bool pk_global_keys() { return G * C <= 32; }
-template <int G, int C> __device__ __forceinline__ int pk_key_base(int gl) {
-  return pk_global_keys<G, C>() ? 31 - C * gl : 31;
-}
+// lane (wider groups extend the key with the lane: see pk_diag)
+__device__ __forceinline__ bool pk_global_keys(int G, int C) { return G * C <= 32; }
+__device__ __forceinline__ int pk_key_base(int G, int C, int gl) { return pk_global_keys(G, C) ? 31 - C * gl : 31; }
 
 // key bytes 31 - t; `zero` is an opaque 0 so the words stay in registers (PRMT operand c)
-template <int G, int C>
-__device__ __forceinline__ void pk_keys(Band16<G, C>& B, int gl, int zero) {
+template <int C>
+__device__ __forceinline__ void pk_keys(Band16<C>& B, int G, int gl, int zero) {
   constexpr int NP = C / 2;
-  const int tb = pk_key_base<G, C>(gl) + zero;
+  const int tb = pk_key_base(G, C, gl) + zero;
 #pragma unroll
   for (int j = 0; j < NP / 2; ++j)
     B.TC[j] = opaque((uint32_t)(tb - 2 * j) | ((uint32_t)(tb - 2 * j - NP) << 8) |
@@ -114,8 +142,8 @@ __device__ __forceinline__ void pk_keys(Band16<G, C>& B, int gl, int zero) {
 }
 
 // window + reservoirs at (ia0, jb0); `rem` blocks until the next refill
-template <int G, int C>
-__device__ __forceinline__ void pk_reload(Band16<G, C>& B, int gl, int rem, const Problem& P) {
+template <int C>
+__device__ __forceinline__ void pk_reload(Band16<C>& B, int gl, int rem, const Problem& P) {
   const int ia = B.ia0 + C * gl, jb = B.jb0 - C * gl;
   const uint64_t aw = load32c(P.PA, B.sa, B.da, ia);
   B.A0 = plane32(aw, 0); B.A1 = plane32(aw, 1);
@@ -152,9 +180,10 @@ __device__ __forceinline__ uint32_t tree16(const uint32_t (&k)[N]) {
 // One anti-diagonal d of parity PAR: V (parity PAR, holds d-2) is updated in place from
 // N (holds d-1).  CHECK: cells with q outside [qlo, qhi] (beyond the matrix) are dead.
 // Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
-template <int G, int C, int PAR, bool CHECK, bool FMA = (XDROP_PK_FMA != 0)>
-__device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<G, C>& B,
-                                             int gl, int qlo, int qhi, const Problem& P, uint32_t (&ch)[C > 16 ? 2 : 1]) {
+template <int C, int PAR, bool CHECK, bool FMA = (XDROP_PK_FMA != 0)>
+__device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<C>& B,
+                                             int G, int gl, int qlo, int qhi, const Problem& P,
+                                             uint32_t (&ch)[C > 16 ? 2 : 1]) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
   const int thr_d = B.thrN;
   const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
@@ -182,16 +211,16 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
   uint32_t seam;
   if constexpr (PAR == 0) {
     uint32_t x = pk::DEAD2;
-    if constexpr (G > 1) { x = __shfl_up_sync(FULL, N[NP - 1], 1, G); if (gl == 0) x = pk::DEAD2; }
+    if (G > 1) { x = __shfl_up_sync(FULL, N[NP - 1], 1, G); if (gl == 0) x = pk::DEAD2; }
     seam = __byte_perm(N[NP - 1], x, 0x1076);            // (left lane's last odd cell, own odd cell NP-1)
   } else {
     uint32_t x = pk::DEAD2;
-    if constexpr (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
+    if (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
     seam = __byte_perm(N[0], x, 0x5432);                 // (own even cell NP, right lane's even cell 0)
   }
   // the hi half of a seam pair may hold a cell with key bits up to 31 (the next lane's cell 0);
   // clear them so the FMA-pipe adds' carries (see below) cannot reach its value bits
-  if constexpr (G > 1 && FMA) seam &= 0xFFE0FFFFu;
+  if (G > 1 && FMA) seam &= 0xFFE0FFFFu;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) ch[c] = 0;
 #pragma unroll
@@ -253,48 +282,57 @@ __device__ __forceinline__ uint32_t pk_dead(const uint32_t (&ch)[C > 16 ? 2 : 1]
   }
 }
 
-template <int G, int C, int PAR, bool CHECK>
-__device__ __forceinline__ void pk_diag(Band16<G, C>& B, int gl, int d, int qlo, int qhi, const Problem& P,
+template <int C, int PAR, bool CHECK>
+__device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int qlo, int qhi, const Problem& P,
                                         const uint32_t (&chc)[C > 16 ? 2 : 1]) {
   uint32_t ch[C > 16 ? 2 : 1];
   uint32_t kk;
-  if constexpr (PAR == 0) kk = pk_cells<G, C, 0, CHECK>(B.E, B.O, B, gl, qlo, qhi, P, ch);
-  else kk = pk_cells<G, C, 1, CHECK>(B.O, B.E, B, gl, qlo, qhi, P, ch);
+  if constexpr (PAR == 0) kk = pk_cells<C, 0, CHECK>(B.E, B.O, B, G, gl, qlo, qhi, P, ch);
+  else kk = pk_cells<C, 1, CHECK>(B.O, B.E, B, G, gl, qlo, qhi, P, ch);
   const int thr_d = B.thrN;
   // key maximum over both halves: both halves of kk2 hold it; the hi half sign-extends
   const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
   const int kl = ((int)kk2) >> 16;                        // lane key: 32 * value + 31 - (local cell)
   // no live cell: kmax is a dead key (< -16128), so vrel <= -505 and neither the threshold nor best
   // can move (thrH_d = best_{<d} - X, so gv <= best - 505); no separate liveness test is needed
-  int vrel, tst;
-  if constexpr (G == 1) {
+  const uint32_t dl = pk_dead<C>(ch, chc);
+  const unsigned lb = ~dl & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  const int tmin_l = (__clz(lb) - (32 - C)) + C * gl;
+  const int tmax_l = (C - __ffs(lb)) + C * gl;
+  int vrel, tst, tmin, tmax;
+  if (G == 1) {
     vrel = kl >> 5;
     tst = 31 - (kl & 31);
-  } else if constexpr (pk_global_keys<G, C>()) {         // window-wide keys: the max is the argmax
-    const int km = gmax<G>(kl);
+    tmin = lb ? tmin_l : EMIN;
+    tmax = lb ? tmax_l : EMAX;
+  } else if (pk_global_keys(G, C)) {                      // window-wide keys: the max is the argmax
+    const int km = gmax_rt(kl, G);
     vrel = km >> 5;
     tst = 31 - (km & 31);
-  } else {                                                // value first, then the lowest lane, then t
-    const int vl = kl >> 5;
-    vrel = gmax<G>(vl);
-    const unsigned ball = __ballot_sync(FULL, vl == vrel);
-    const int grp = (threadIdx.x & 31) / G;
-    const unsigned gb = (G == 32) ? ball : ((ball >> (grp * G)) & ((1u << G) - 1u));
-    const int first = __ffs(gb) - 1;
-    tst = __shfl_sync(FULL, C * gl + 31 - (kl & 31), first, G);
+    tmin = gmin_rt(lb ? tmin_l : EMIN, G);
+    tmax = gmax_rt(lb ? tmax_l : EMAX, G);
+  } else {
+    // 32-bit group key: value, then the lowest lane, then the lowest local cell (reading Q8:
+    // smallest i); the live extents travel as one 16x2 word (tmax, 0x7FFF - tmin; -1 = none)
+    int K = (int)((uint32_t)(kl >> 5) << 10) | ((31 - gl) << 5) | (kl & 31);
+    uint32_t ex = lb ? (((uint32_t)tmax_l << 16) | (uint32_t)(0x7FFF - tmin_l)) : 0xFFFFFFFFu;
+    if (G == 32) K = __reduce_max_sync(FULL, K);
+    for (int o = 1; o < G; o <<= 1) {
+      if (G < 32) K = max(K, __shfl_xor_sync(FULL, K, o));
+      ex = __vmaxs2(ex, __shfl_xor_sync(FULL, ex, o));
+    }
+    vrel = K >> 10;
+    tst = C * (31 - ((K >> 5) & 31)) + 31 - (K & 31);
+    const int hx = ((int)ex) >> 16, lx = (int)(int16_t)(ex & 0xffffu);
+    tmax = hx < 0 ? EMAX : hx;
+    tmin = lx < 0 ? EMIN : 0x7FFF - lx;
   }
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
   B.thrN = thr_d + max(0, vrel - P.X) - P.g;
   // ---- off the critical path: live extent, best / argmax, hull count (garbage in inactive
   // lanes is harmless: their state is never written out)
-  const uint32_t dl = pk_dead<C>(ch, chc);
-  const unsigned lb = ~dl & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
   const int ibase = (d + B.K0 + PAR) >> 1;
-  int tmin = (__clz(lb) - (32 - C)) + C * gl;
-  int tmax = (C - __ffs(lb)) + C * gl;
-  tmin = gmin<G>(lb ? tmin : EMIN);
-  tmax = gmax<G>(lb ? tmax : EMAX);
   const int mn = (tmin == EMIN) ? EMIN : ibase + tmin;
   const int mx = (tmax == EMAX) ? EMAX : ibase + tmax;
   const int woff = -P.g * (d - B.dbase);
@@ -340,11 +378,11 @@ __device__ __forceinline__ void pk_shift_arr(uint32_t (&A)[NP]) {
   for (int u = 0; u < NP; ++u) A[u] = T[u];
 }
 template <int C, int K>
-__device__ __forceinline__ void pk_shift_k(Band16<1, C>& B) {
+__device__ __forceinline__ void pk_shift_k(Band16<C>& B) {
   pk_shift_arr<C / 2, K>(B.E); pk_shift_arr<C / 2, K>(B.O);
 }
 template <int C>
-__device__ __forceinline__ void pk_shift_n(Band16<1, C>& B, int s) {
+__device__ __forceinline__ void pk_shift_n(Band16<C>& B, int s) {
   switch (s) {
     case 1: pk_shift_k<C, 1>(B); break;   case -1: pk_shift_k<C, -1>(B); break;
     case 2: pk_shift_k<C, 2>(B); break;   case -2: pk_shift_k<C, -2>(B); break;
@@ -358,9 +396,9 @@ __device__ __forceinline__ void pk_shift_n(Band16<1, C>& B, int s) {
   }
 }
 // group mode: shift by one cell (dir = +1: cell t <- t + 1), across the group's lanes
-template <int G, int NP>
-__device__ __forceinline__ void pk_shift1(uint32_t (&A)[NP], int gl, int dir) {
-  const unsigned gm = group_mask<G>();
+template <int NP>
+__device__ __forceinline__ void pk_shift1(uint32_t (&A)[NP], int G, int gl, int dir) {
+  const unsigned gm = gmask(G);
   if (dir > 0) {
     uint32_t x = __shfl_down_sync(gm, A[0], 1, G);
     if (gl == G - 1) x = pk::DEAD2;
@@ -388,13 +426,12 @@ __device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP], int kb) {
 }
 
 // checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
-template <int G, int C>
-__device__ __forceinline__ void pk_save(const Band16<G, C>& B, int gl, int d, const Esc& e) {
+template <int C>
+__device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d, const Esc& e) {
   constexpr int NP = C / 2;
-  const unsigned gm = group_mask<G>();
   int slot = 0;
   if (gl == 0) slot = atomicAdd(e.pool_tail, 1);
-  if constexpr (G > 1) slot = __shfl_sync(gm, slot, 0, G);
+  if (G > 1) slot = __shfl_sync(gmask(G), slot, 0, G);
   if (slot >= e.cap) {
     if (gl == 0) push_item(e.fb_items, e.fb_tail, B.item);
     return;
@@ -404,7 +441,7 @@ __device__ __forceinline__ void pk_save(const Band16<G, C>& B, int gl, int d, co
     rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrN; rec[5] = B.best;
     rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
     rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = G * C;
-    rec[15] = B.cells; rec[16] = 0;
+    rec[15] = B.cells; rec[16] = 0; rec[REC_T] = rec_stamp();
   }
 #pragma unroll
   for (int u = 0; u < NP; ++u) {
@@ -418,15 +455,15 @@ __device__ __forceinline__ void pk_save(const Band16<G, C>& B, int gl, int d, co
     }
   }
   __threadfence();
-  if constexpr (G > 1) __syncwarp(gm);
+  if (G > 1) __syncwarp(gmask(G));
   if (gl == 0) push_item(e.q, e.q_tail, slot);
 }
 
 // end of a block of two anti-diagonals (as band_block_end<G, C>)
-template <int G, int C>
-__device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int& rem, const Problem& P, int level,
-                                             const Esc& esc) {
-  constexpr int S = G * C;
+template <int C>
+__device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d, int& rem, const Problem& P,
+                                             int level, const Esc& esc) {
+  const int S = G * C;
   if (d - B.dbase >= 1024) {      // keep W bounded for the 32-bit tiers' checkpoints
     const int woff = -P.g * (d - B.dbase);
     B.thrD1 -= woff; B.thrD -= woff; B.thrN -= woff;
@@ -456,12 +493,12 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
   int qmn = 1 << 30, qmx = -(1 << 30);
   if (!e0) { qmn = 2 * B.minL1 - d - B.K0; qmx = 2 * B.maxL1 - d - B.K0; }
   if (!e1) { qmn = min(qmn, 2 * B.minL2 - (d - 1) - B.K0); qmx = max(qmx, 2 * B.maxL2 - (d - 1) - B.K0); }
-  if constexpr (G == 1) {
+  if (G == 1) {
     if (qmx >= 2 * S - 2 || qmn <= 1) {
       const int s_lo = (qmx - 2 * S + 4) >> 1;
       const int s_hi = (qmn - 2) >> 1;
       if (s_lo > s_hi) {
-        pk_save<G, C>(B, gl, d, esc);
+        pk_save<C>(B, G, gl, d, esc);
         B.active = false;
         return;
       }
@@ -470,9 +507,9 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
       sh = min(max(sh, -8), 8);
       if (sh == 0) sh = s_lo > 0 ? s_lo : s_hi;
       pk_shift_n<C>(B, sh);
-      pk_rekey<C / 2>(B.E, pk_key_base<G, C>(gl)); pk_rekey<C / 2>(B.O, pk_key_base<G, C>(gl));
+      pk_rekey<C / 2>(B.E, pk_key_base(G, C, gl)); pk_rekey<C / 2>(B.O, pk_key_base(G, C, gl));
       B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
-      pk_reload<G, C>(B, gl, rem, P);
+      pk_reload<C>(B, gl, rem, P);
     }
   } else {
     int dir = 0;
@@ -480,22 +517,22 @@ __device__ __forceinline__ void pk_block_end(Band16<G, C>& B, int gl, int d, int
     if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
     else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
     if (ovf) {
-      pk_save<G, C>(B, gl, d, esc);
+      pk_save<C>(B, G, gl, d, esc);
       B.active = false;
       return;
     }
     if (dir != 0) {
-      pk_shift1<G, C / 2>(B.E, gl, dir); pk_shift1<G, C / 2>(B.O, gl, dir);
-      pk_rekey<C / 2>(B.E, pk_key_base<G, C>(gl)); pk_rekey<C / 2>(B.O, pk_key_base<G, C>(gl));
+      pk_shift1<C / 2>(B.E, G, gl, dir); pk_shift1<C / 2>(B.O, G, gl, dir);
+      pk_rekey<C / 2>(B.E, pk_key_base(G, C, gl)); pk_rekey<C / 2>(B.O, pk_key_base(G, C, gl));
       B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
-      pk_reload<G, C>(B, gl, rem, P);
+      pk_reload<C>(B, gl, rem, P);
     }
   }
 }
 
 // key-byte part of the PRMT-mask chains (pk_dead subtracts it)
-template <int G, int C>
-__device__ __forceinline__ void pk_chain_consts(const Band16<G, C>& B, uint32_t (&chc)[C > 16 ? 2 : 1]) {
+template <int C>
+__device__ __forceinline__ void pk_chain_consts(const Band16<C>& B, uint32_t (&chc)[C > 16 ? 2 : 1]) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
@@ -510,46 +547,60 @@ __device__ __forceinline__ void pk_chain_consts(const Band16<G, C>& B, uint32_t 
   }
 }
 
-// anti-diagonal loop (from an even d; groups of a warp may sit at different d)
-template <int G, int C>
-__device__ __forceinline__ void pk_loop(Band16<G, C>& B, int gl, int d, const Problem& P, int level, const Esc& esc,
-                                        const Steal* st) {
-  constexpr int S = G * C;
-  uint32_t chc[C > 16 ? 2 : 1];
-  pk_chain_consts<G, C>(B, chc);
-  int rem = 16, blk = 0;
-  pk_reload<G, C>(B, gl, rem, P);
-  while (__any_sync(FULL, B.active)) {
-    if (G == 1 && st != nullptr && ((++blk & 31) == 0)) {
-      int go = 0;
-      if ((threadIdx.x & 31) == 0) go = ld_volatile(st->idle) >= st->thresh;
-      go = __shfl_sync(FULL, go, 0);
-      if (go && B.active) {
-        const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
-        const int left = 2 * min(B.m - ic, B.n - (d - ic));
-        if (left >= st->min_rem) {
-          pk_save<G, C>(B, gl, d, st->es);
-          B.active = false;
-        }
-      }
-      if (!__any_sync(FULL, B.active)) break;
+// two anti-diagonals (d+1, d+2) and the block end; boundary masking only when some group needs it
+template <int C>
+__device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int& rem, const Problem& P, int level,
+                                        const Esc& esc, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
+  const int S = G * C;
+  const int d2 = d + 2;
+  const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
+  if (__any_sync(FULL, need)) {
+    pk_diag<C, 1, true>(B, G, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
+    pk_diag<C, 0, true>(B, G, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
+  } else {
+    pk_diag<C, 1, false>(B, G, gl, d + 1, 0, 0, P, chc);
+    pk_diag<C, 0, false>(B, G, gl, d2, 0, 0, P, chc);
+  }
+  d = d2;
+  pk_block_end<C>(B, G, gl, d, rem, P, level, esc);
+}
+
+// tail stealing check (lane mode): once enough warps idle, checkpoint this lane's extension to
+// the steal queue if it still has >= min_rem anti-diagonals ahead
+template <int C>
+__device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st) {
+  int go = 0;
+  if ((threadIdx.x & 31) == 0) go = ld_volatile(st.idle) >= st.thresh;
+  go = __shfl_sync(FULL, go, 0);
+  if (go && B.active) {
+    const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
+    const int left = 2 * min(B.m - ic, B.n - (d - ic));
+    if (left >= st.min_rem) {
+      pk_save<C>(B, G, gl, d, st.es);
+      B.active = false;
     }
-    const int d2 = d + 2;
-    const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
-    if (__any_sync(FULL, need)) {
-      pk_diag<G, C, 1, true>(B, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
-      pk_diag<G, C, 0, true>(B, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
-    } else {
-      pk_diag<G, C, 1, false>(B, gl, d + 1, 0, 0, P, chc);
-      pk_diag<G, C, 0, false>(B, gl, d2, 0, 0, P, chc);
-    }
-    d = d2;
-    pk_block_end<G, C>(B, gl, d, rem, P, level, esc);
   }
 }
 
-template <int G, int C>
-__device__ __forceinline__ void pk_geom(Band16<G, C>& B, const Problem& P, int item) {
+// anti-diagonal loop (from an even d; groups of a warp may sit at different d)
+template <int C>
+__device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, const Problem& P, int level,
+                                        const Esc& esc, const Steal* st) {
+  uint32_t chc[C > 16 ? 2 : 1];
+  pk_chain_consts<C>(B, chc);
+  int rem = 16, blk = 0;
+  pk_reload<C>(B, gl, rem, P);
+  while (__any_sync(FULL, B.active)) {
+    if (G == 1 && st != nullptr && ((++blk & 31) == 0)) {
+      pk_steal<C>(B, G, gl, d, *st);
+      if (!__any_sync(FULL, B.active)) break;
+    }
+    pk_step<C>(B, G, gl, d, rem, P, level, esc, chc);
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void pk_geom(Band16<C>& B, const Problem& P, int item) {
   if (item >= 0) {
     B.active = true; B.item = item;
     const Geom gm = item_geom(P, B.item);
@@ -561,25 +612,23 @@ __device__ __forceinline__ void pk_geom(Band16<G, C>& B, const Problem& P, int i
   }
 }
 
-// Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
-template <int G, int C>
-__device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
-                                       const Steal* st = nullptr) {
-  constexpr int S = G * C, NP = C / 2;
-  static_assert(S <= 32 && C % 4 == 0 && NP <= 16, "packed window from a seed");
-  const int gl = (threadIdx.x & 31) % G;
-  Band16<G, C> B;
-  pk_geom<G, C>(B, P, item);
-  pk_keys<G, C>(B, gl, P.keym >> 8);
+// Group state of a fresh extension at its seed (item < 0: idle group); window S = G*C <= 32.
+template <int C>
+__device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int item, const Problem& P) {
+  constexpr int NP = C / 2;
+  const int S = G * C;
+  pk_geom<C>(B, P, item);
   B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1;
 #pragma unroll
   for (int u = 0; u < NP; ++u) { B.E[u] = pk::DEAD2; B.O[u] = pk::DEAD2; }
   // origin: d = 0, k = 0 -> even cell S/2 (lane (S/2) / C, local cell tl), relative to thrW_0 = BIAS - X
   {
-    constexpr int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
+    const int tl = (S / 2) % C, u0 = tl % NP, h0 = tl / NP;
     if (gl == (S / 2) / C) {
-      const uint32_t v0 = (uint32_t)(32 * P.X + pk_key_base<G, C>(gl) - tl) & 0xffffu;
-      B.E[u0] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
+      const uint32_t v0 = (uint32_t)(32 * P.X + pk_key_base(G, C, gl) - tl) & 0xffffu;
+#pragma unroll
+      for (int u = 0; u < NP; ++u)
+        if (u == u0) B.E[u] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
     }
   }
   B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
@@ -587,29 +636,39 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
   if (B.active && B.m + B.n == 0) {
     if (gl == 0) {
-      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+      ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = 0; o.cells = 1; o.pad = 0;
       P.ext[B.item] = o;
     }
     B.active = false;
   }
-  pk_loop<G, C>(B, gl, 0, P, level, esc, st);
 }
 
-// Resume one checkpointed extension per group (rec == nullptr: idle group) from a 32-bit record
-// (band_save / pk_save format) in a window of S = G*C >= the record's; the old window lands in the
-// middle.  Stored values become relative to a reference T per anti-diagonal with every live W >= T
-// and W - T <= X + M:  T_d = min(thrW_{d+1} + g, min live W_d), T_{d-1} = min(thrW_{d+1} + 2g, min
-// live W_{d-1}) (the true thresholds satisfy thr_d <= thrW_{d+1} + g, thr_{d-1} <= thr_d + g, and
-// live values exceed their threshold by at most X + M).  The recurrence only needs differences of
-// the references, so any such T is exact.
+// Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
 template <int G, int C>
-__device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int level, const Esc& esc) {
-  constexpr int S = G * C, NP = C / 2;
+__device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
+                                       const Steal* st = nullptr) {
+  static_assert(G * C <= 32 && C % 4 == 0 && C / 2 <= 16, "packed window from a seed");
   const int gl = (threadIdx.x & 31) % G;
-  Band16<G, C> B;
-  int d = 0;
-  pk_geom<G, C>(B, P, rec ? rec[0] : -1);
-  pk_keys<G, C>(B, gl, P.keym >> 8);
+  Band16<C> B;
+  pk_keys<C>(B, G, gl, P.keym >> 8);
+  pk_init_seed<C>(B, G, gl, item, P);
+  pk_loop<C>(B, G, gl, 0, P, level, esc, st);
+}
+
+// Group state from a checkpoint record (rec == nullptr: idle group) in a window of S = G*C >= the
+// record's; the old window lands in the middle.  Stored values become relative to a reference T per
+// anti-diagonal with every live W >= T and W - T <= X + M:  T_d = min(thrW_{d+1} + g, min live W_d),
+// T_{d-1} = min(thrW_{d+1} + 2g, min live W_{d-1}) (the true thresholds satisfy
+// thr_d <= thrW_{d+1} + g, thr_{d-1} <= thr_d + g, and live values exceed their threshold by at
+// most X + M).  The recurrence only needs differences of the references, so any such T is exact.
+// Group-local: only the lanes of this group take part (a refilling pool calls it for some groups).
+template <int C>
+__device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int& d, const int* rec,
+                                               const Problem& P) {
+  constexpr int NP = C / 2;
+  const int S = G * C;
+  d = 0;
+  pk_geom<C>(B, P, rec ? rec[0] : -1);
   int w_e[C], w_o[C];                                    // this lane's cells: even (d), odd (d-1)
   if (rec) {
     d = rec[1];
@@ -637,21 +696,123 @@ __device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int 
     if (w_e[t] > 0) me = min(me, w_e[t]);
     if (w_o[t] > 0) mo = min(mo, w_o[t]);
   }
-  me = gmin<G>(me); mo = gmin<G>(mo);
+  me = gmin_grp(me, G); mo = gmin_grp(mo, G);
   B.thrD = min(B.thrN + P.g, me);
   B.thrD1 = min(B.thrN + 2 * P.g, mo);
+  const int kb = pk_key_base(G, C, gl);
 #pragma unroll
   for (int u = 0; u < NP; ++u) {
     uint32_t e = 0, o = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int t = u + NP * h;
-      const uint32_t tc = pk_key_base<G, C>(gl) - t;
+      const uint32_t tc = kb - t;
       const uint32_t ve = w_e[t] > 0 ? ((uint32_t)(32 * (w_e[t] - B.thrD)) | tc) & 0xffffu : 0xC000u | tc;
       const uint32_t vo = w_o[t] > 0 ? ((uint32_t)(32 * (w_o[t] - B.thrD1)) | tc) & 0xffffu : 0xC000u | tc;
       e |= ve << (16 * h); o |= vo << (16 * h);
     }
     B.E[u] = e; B.O[u] = o;
   }
-  pk_loop<G, C>(B, gl, d, P, level, esc, nullptr);
+}
+
+// Resume one checkpointed extension per group (rec == nullptr: idle group).  Warp-collective.
+template <int G, int C>
+__device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int level, const Esc& esc) {
+  const int gl = (threadIdx.x & 31) % G;
+  Band16<C> B;
+  int d = 0;
+  pk_keys<C>(B, G, gl, P.keym >> 8);
+  pk_resume_init<C>(B, G, gl, d, rec, P);
+  pk_loop<C>(B, G, gl, d, P, level, esc, nullptr);
+}
+
+// A tier of pk_merged_kernel's shared loop, read from device memory where used (rare paths), so
+// the queue descriptors take no registers in the loop.
+struct PkTier {
+  Esc src;          // records this tier resumes (pool tiers)
+  Esc esc;          // where its extensions that outgrow the window are checkpointed
+  int* head;        // claim head of src's queue
+  int* done;        // ended extensions of this tier (nullptr: not counted)
+  int level;        // reported level of extensions that end here
+};
+
+// take up to k claimed records (queue index h..) into the idle groups of the warp (warp-collective)
+template <int C>
+__device__ __forceinline__ void pk_take(Band16<C>& B, int G, int gl, int& d, int& rem, const Esc& src, int h, int k,
+                                        const Problem& P) {
+  const int lane = threadIdx.x & 31;
+  const unsigned idle = __ballot_sync(FULL, !B.active && gl == 0);
+  const int rank = __popc(idle & ((1u << (lane & ~(G - 1))) - 1u));
+  if (!B.active && rank < k) {                           // group-uniform
+    int slot = -1;
+    if (gl == 0) slot = wait_entry(src.q, h + rank);
+    slot = __shfl_sync(gmask(G), slot, 0, G);
+    pk_resume_init<C>(B, G, gl, d, src.pool + (size_t)slot * src.rec_ints, P);
+    rem = 16;
+    pk_reload<C>(B, gl, rem, P);
+  }
+}
+
+// One work unit of pk_merged_kernel's shared C = 32 loop, with the lanes per extension G chosen at
+// run time (one instance serves every tier, so the hot code stays in the instruction cache):
+//  tier 0 (fresh): 32 fresh extensions, G = 1, items[base + lane]; lane-mode tail stealing
+//  tier 1, 2 (pool): a refilling resume pool (T1: G = 4, T2: G = 8): the 32/G groups start with the
+//        k records of tiers[t].src at queue index h; a group whose extension ends (result written,
+//        or checkpointed to tiers[t].esc) takes the next queued record at the next refill point
+//        (every 8 blocks; at once when the whole warp is idle).  The records taken are added to
+//        *tiers[t].done when the unit returns (after every checkpoint it wrote is published).
+// Loop-carried state beyond the extension's is kept to a few registers (the loop runs at the
+// 168-register cap of 3 blocks per SM, where every extra live value costs instructions).
+template <int C>
+__device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const PkTier* tiers, const int* items,
+                                        int base, int n_items, int h, int k, const Steal& st) {
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+  Band16<C> B;
+  pk_keys<C>(B, G, gl, P.keym >> 8);
+  uint32_t chc[C > 16 ? 2 : 1];
+  pk_chain_consts<C>(B, chc);
+  int d = 0, rem = 16;
+  int taken = k;                                         // pool: records claimed (lane 0)
+  if (t == 0) {
+    const int slot = base + lane;
+    pk_init_seed<C>(B, 1, 0, slot < n_items ? items[slot] : -1, P);
+    pk_reload<C>(B, gl, rem, P);
+  } else {
+    pk_resume_init<C>(B, G, gl, d, nullptr, P);
+    pk_take<C>(B, G, gl, d, rem, tiers[t].src, h, k, P);
+  }
+  for (int blk = 1;; ++blk) {
+    if (t != 0) {
+      const bool any = __any_sync(FULL, B.active);
+      if (!any || (blk & 7) == 0) {
+        const unsigned idle = __ballot_sync(FULL, !B.active && gl == 0);
+        int kk = 0;
+        if (idle) {
+          int hh = 0;
+          if (lane == 0) hh = claim(tiers[t].head, tiers[t].src.q_tail, __popc(idle), true, kk);
+          kk = __shfl_sync(FULL, kk, 0);
+          if (kk) {
+            hh = __shfl_sync(FULL, hh, 0);
+            taken += kk;
+            pk_take<C>(B, G, gl, d, rem, tiers[t].src, hh, kk, P);
+          }
+        }
+        if (!any && kk == 0) {
+          int* done = tiers[t].done;
+          if (done != nullptr) {
+            __syncwarp();
+            if (lane == 0) { __threadfence(); atomicAdd(done, taken); }
+          }
+          return;
+        }
+      }
+    } else if ((blk & 31) == 0) {
+      pk_steal<C>(B, 1, gl, d, st);
+    }
+    if (!__any_sync(FULL, B.active)) {
+      if (t != 0) continue;                              // report and refill (or return) above
+      return;
+    }
+    pk_step<C>(B, G, gl, d, rem, P, tiers[t].level, tiers[t].esc, chc);
+  }
 }

@@ -27,10 +27,12 @@ def xsweep_small():
                                 6.0, 5_000, k=17, X=15, f_sp=0.2)
 
 
+@pytest.mark.parametrize("flags", [8, 16])
 @pytest.mark.parametrize("X", [15, 50, 100])
-def test_xsweep_small_all_pairs(xd, xsweep_small, X):
+def test_xsweep_small_all_pairs(xd, xsweep_small, X, flags):
+    """Both packed band kernels (tiered / shared)."""
     w = xsweep_small.with_X(X)
-    with xd.Aligner() as al:
+    with xd.Aligner(flags=flags) as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
         st = al.stats()
     ref, rcells = oracle_of(w, X=X)
@@ -50,12 +52,38 @@ def test_xsweep_full_size_sampled(xd):
     assert_same(res[idx], cells[idx], ref, rcells, "xsweep full sampled")
 
 
-def test_celegans_shaped_small(xd):
-    """BASELINE configs[4] recipe (lognormal 2-40 kb, f_sp = 0.1) at 1/2000 scale."""
+@pytest.mark.parametrize("flags", [0, 8, 16])
+def test_celegans_shaped_small(xd, flags):
+    """BASELINE configs[4] recipe (lognormal 2-40 kb, f_sp = 0.1) at 1/2000 scale, per-call kernel
+    choice and both packed kernels forced."""
     from synth import workload as W
     w = W.make_pool_workload("celegans-small", 55, 600_000, 400, W._lognormal_len(8_000, 0.6, 2_000, 40_000),
                              8.0, 1_000, k=17, X=15, f_sp=0.1)
-    with xd.Aligner() as al:
+    with xd.Aligner(flags=flags) as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=15)
     ref, rcells = oracle_of(w)
-    assert_same(res, cells, ref, rcells, "celegans small")
+    assert_same(res, cells, ref, rcells, f"celegans small flags={flags}")
+
+
+def test_celegans_scaled_sample_shared_kernel_chosen(xd):
+    """Config 5 at 1/20 scale (200k pairs): the second call runs the shared kernel (the first call's
+    T0 -> T1 checkpoints exceed twice the resident T1 groups); a stratified sample (every 400th pair
+    plus the 100 with the longest extensions) is bit-exact against the oracle, and both calls agree."""
+    import torch
+    from synth import workload as W
+    w = W.config("celegans", scale=0.05)
+    with xd.Aligner() as al:
+        r1, c1 = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        k1 = al.stats()["band_kernel"]
+        r2, c2 = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
+    assert np.array_equal(r1, r2) and np.array_equal(c1, c2)
+    assert k1 == "tiered"
+    groups = torch.cuda.get_device_properties(0).multi_processor_count * 3 * 4 * 8
+    assert st["escalated"][0] >= 2 * groups and st["band_kernel"] == "shared", (st["escalated"], st["band_kernel"])
+    L = np.diff(w.offsets)
+    la, lb = L[w.pairs[:, 0]], L[w.pairs[:, 1] & 0x7fffffff]
+    ext = np.minimum(w.pairs[:, 2], w.pairs[:, 3]) + np.minimum(la - w.pairs[:, 2], lb - w.pairs[:, 3])
+    idx = np.unique(np.concatenate([np.arange(0, w.n_pairs, 400), np.argsort(-ext)[:100]]))
+    ref, rcells = oracle_of(w, pairs=w.pairs[idx])
+    assert_same(r2[idx], c2[idx], ref, rcells, "celegans x0.05 sampled")

@@ -44,7 +44,7 @@ def test_cfg1_full(xd):
     assert_same(res, cells, ref, rcells, "cfg1")
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 4])
+@pytest.mark.parametrize("flags", [0, 1, 2, 4, 8, 16])
 @pytest.mark.parametrize("X", [0, 1, 5, 15, 50])
 def test_random_edge_cases_all_paths(xd, flags, X):
     from synth import workload as W
@@ -320,10 +320,16 @@ def test_packed_range_gate_and_negative_mismatch(xd, M, mu, g, X):
 
 @pytest.mark.parametrize("env", [{"XDROP_PK16": "0"}, {"XDROP_OCC": "1"},
                                  {"XDROP_T0_PER_SM": "1", "XDROP_IDLE_NS": "0"},
-                                 {"XDROP_LONG_G": "2", "XDROP_LONG_ALPHA": "0.001"}])
+                                 {"XDROP_LONG_G": "2", "XDROP_LONG_ALPHA": "0.001"},
+                                 {"XDROP_KERNEL": "1"}, {"XDROP_KERNEL": "2"},
+                                 {"XDROP_KERNEL": "2", "XDROP_LONG_G": "2", "XDROP_LONG_ALPHA": "0.001"},
+                                 {"XDROP_KERNEL": "2", "XDROP_OCC": "1", "XDROP_AGE_US": "0"},
+                                 {"XDROP_KERNEL": "2", "XDROP_STEAL_MIN": "16", "XDROP_LONG_G": "0"}])
 def test_kernel_variants_identical(xd, env, monkeypatch):
     """32-bit vs packed T0, 1 block/SM, 1 T0 block/SM (the rest escalation-only), packed 2-lane long
-    mode: every variant gives the oracle's results on an escalating, strand-mixed batch."""
+    mode, the tiered and the shared packed kernels (the shared one also with 2-lane
+    long mode, one block per SM and immediate partial claims, and with tail stealing): every variant
+    gives the oracle's results on an escalating, strand-mixed batch."""
     from synth import workload as W
     for k_, v in env.items():
         monkeypatch.setenv(k_, v)
@@ -335,17 +341,20 @@ def test_kernel_variants_identical(xd, env, monkeypatch):
     assert_same(res, cells, ref, rcells, f"variant {env}")
 
 
-def test_packed_resume_reaches_s1024(xd):
-    """Unrelated continuations at X = 400 (packed path: X + M <= 510) outgrow T0 (32 cells), T1 (64)
-    and T2 (256): checkpoints resume in the packed 16-bit tiers up to the S = 1024 kernel, exactly."""
+@pytest.mark.parametrize("flags", [8, 16])
+def test_packed_resume_reaches_s1024(xd, flags):
+    """Unrelated continuations at X = 400 (packed path: X + M <= 510) outgrow T0 (32 cells), T1 (64
+    tiered / 128 shared) and T2 (256): checkpoints resume in the packed 16-bit tiers up to the
+    S = 1024 kernel, exactly, in both packed kernels."""
     from synth import workload as W
     w = W.random_pairs_workload(seed=660, n_pairs=24, len_lo=2500, len_hi=4000, k=11, X=400, related=0.0)
-    with xd.Aligner() as al:
+    with xd.Aligner(flags=flags) as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
         st = al.stats()
     ref, rcells = oracle_of(w)
-    assert_same(res, cells, ref, rcells, "packed resume S1024")
+    assert_same(res, cells, ref, rcells, f"packed resume S1024 flags={flags}")
     assert st["escalated"][2] > 0, st["escalated"]
+    assert st["band_kernel"] == ("tiered" if flags == 8 else "shared")
 
 
 def test_random_scoring_sweep_packed_and_32bit(xd):

@@ -13,8 +13,8 @@ with xd.Aligner() as al:
     tl = al.timeline(); st = al.stats()
 t0 = tl[:, 2].min(); T = (tl[:, 3].max() - t0) / 1e6
 print(f"kernel span {T:.2f} ms, units {len(tl)}, stolen {st['stolen']}, band ms {st['level_ms'][0]:.2f}")
-names = ["lane", "long", "stolen", "pair", "warp", "endgame"]
-for ty in range(6):
+names = ["lane", "long", "stolen", "pair", "warp", "endgame", "wide"]
+for ty in range(7):
     m = tl[:, 0] == ty
     if m.any():
         d = (tl[m, 3] - tl[m, 2]) / 1e6
