@@ -259,7 +259,10 @@ def run_native(args, world, rank, local):
     lvl_ms = np.mean([s["level_ms"] for s in stats], axis=0)
     lvl_cells = stats[-1]["level_cells"]
     dom = int(np.argmax(lvl_ms))
-    dom_names = ["xk::band_merged_kernel<32,4,8,PK> (T0 packed 16x2 lane/4-lane modes + T1/T2 in-kernel escalation)",
+    band_kernel = stats[-1].get("band_kernel", "tiered")
+    dom_names = [{"tiered": "xk::pk_tiered_kernel<4,8> (T0 packed 16x2 lane/4-lane modes + T1/T2 in-kernel escalation)",
+                  "shared": "xk::pk_merged_kernel<4,8> (one run-time-G packed loop for T0/T1/T2 + 4-lane units)",
+                  "merged32": "xk::band_merged_kernel<32,4,8> (32-bit cells)"}[band_kernel],
                  "(merged into level 0)",
                  "xk::band_kernel<32,32> (warp/extension)", "xk::general_kernel"]
     achieved_ops = lvl_cells[dom] * ALGO_OPS_PER_CELL / (lvl_ms[dom] * 1e-3)
@@ -286,7 +289,10 @@ def run_native(args, world, rank, local):
     try:
         p_alu, p_dual = al.int32_peak()
         roofline["measured_int32_issue"] = {"alu_only_gops": round(p_alu / 1e9, 1),
-                                            "alu_plus_fma_gops": round(p_dual / 1e9, 1)}
+                                            "alu_plus_fma_gops": round(p_dual / 1e9, 1),
+                                            "note": "source-level int ops/s of int32_peak_kernel; ptxas routes ~40% "
+                                                    "of its adds to IMAD/VIADD on the FMA pipe, so this is an "
+                                                    "ALU+FMA rate, not a bound on the ALU pipe alone"}
     except Exception:
         pass
 

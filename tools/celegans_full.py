@@ -32,13 +32,14 @@ def main():
         for _ in range(3):
             res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
             st = al.stats()
-            ts.append((st["total_ms"], st["level_ms"]))
+            ts.append((st["total_ms"], st["level_ms"], st["band_kernel"]))
     best = min(ts, key=lambda x: x[0])
     tot = float(cells.sum())
-    lines += ["| pairs | cells | device ms | GCUPS | alignments/s | tier ms (T0-2 / S1024 / - / unbounded) | checkpoints |",
-              "|---|---|---|---|---|---|---|",
+    lines += ["| pairs | cells | device ms | GCUPS | alignments/s | tier ms (T0-2 / S1024 / - / unbounded) | checkpoints | band kernel |",
+              "|---|---|---|---|---|---|---|---|",
               f"| {p.shape[0]} | {tot:.3e} | {best[0]:.1f} | {tot / best[0] / 1e6:.1f} | {p.shape[0] / best[0] * 1e3:.3e} | "
-              f"{'/'.join('%.1f' % x for x in best[1])} | {st['escalated']} |", ""]
+              f"{'/'.join('%.1f' % x for x in best[1])} | {st['escalated']} | {best[2]} |", "",
+              "calls (device ms, kernel): " + ", ".join(f"{t[0]:.1f} {t[2]}" for t in ts), ""]
     # stratified oracle sample: every 100th pair in cost order + the 1,000 longest
     import oracle
     lens = np.diff(w.offsets)
