@@ -315,17 +315,22 @@ __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int 
     // 32-bit group key: value, then the lowest lane, then the lowest local cell (reading Q8:
     // smallest i); the live extents travel as one 16x2 word (tmax, 0x7FFF - tmin; -1 = none)
     int K = (int)((uint32_t)(kl >> 5) << 10) | ((31 - gl) << 5) | (kl & 31);
-    uint32_t ex = lb ? (((uint32_t)tmax_l << 16) | (uint32_t)(0x7FFF - tmin_l)) : 0xFFFFFFFFu;
-    if (G == 32) K = __reduce_max_sync(FULL, K);
-    for (int o = 1; o < G; o <<= 1) {
-      if (G < 32) K = max(K, __shfl_xor_sync(FULL, K, o));
-      ex = __vmaxs2(ex, __shfl_xor_sync(FULL, ex, o));
+    if (G == 32) {                                        // CREDUX: one instruction per reduction
+      K = __reduce_max_sync(FULL, K);
+      tmin = __reduce_min_sync(FULL, lb ? tmin_l : EMIN);
+      tmax = __reduce_max_sync(FULL, lb ? tmax_l : EMAX);
+    } else {
+      uint32_t ex = lb ? (((uint32_t)tmax_l << 16) | (uint32_t)(0x7FFF - tmin_l)) : 0xFFFFFFFFu;
+      for (int o = 1; o < G; o <<= 1) {
+        K = max(K, __shfl_xor_sync(FULL, K, o));
+        ex = __vmaxs2(ex, __shfl_xor_sync(FULL, ex, o));
+      }
+      const int hx = ((int)ex) >> 16, lx = (int)(int16_t)(ex & 0xffffu);
+      tmax = hx < 0 ? EMAX : hx;
+      tmin = lx < 0 ? EMIN : 0x7FFF - lx;
     }
     vrel = K >> 10;
     tst = C * (31 - ((K >> 5) & 31)) + 31 - (K & 31);
-    const int hx = ((int)ex) >> 16, lx = (int)(int16_t)(ex & 0xffffu);
-    tmax = hx < 0 ? EMAX : hx;
-    tmin = lx < 0 ? EMIN : 0x7FFF - lx;
   }
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
@@ -464,11 +469,6 @@ template <int C>
 __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d, int& rem, const Problem& P,
                                              int level, const Esc& esc) {
   const int S = G * C;
-  if (d - B.dbase >= 1024) {      // keep W bounded for the 32-bit tiers' checkpoints
-    const int woff = -P.g * (d - B.dbase);
-    B.thrD1 -= woff; B.thrD -= woff; B.thrN -= woff;
-    B.dbase = d;
-  }
   if (--rem == 0) {
     rem = 16;
     if (B.active) {
@@ -527,6 +527,18 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
       B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
       pk_reload<C>(B, gl, rem, P);
     }
+  }
+}
+
+// keep W (= offset-space values of the 32-bit record format) bounded: rebase every >= 1024
+// anti-diagonals.  Called from the loops' every-32-blocks branch (warp-uniform), so d - dbase stays
+// below 1024 + 64: |W| and the 32-bit tiers' argmax keys W * 128 stay far inside int32.
+template <int C>
+__device__ __forceinline__ void pk_rebase(Band16<C>& B, int d, const Problem& P) {
+  if (d - B.dbase >= 1024) {
+    const int woff = -P.g * (d - B.dbase);
+    B.thrD1 -= woff; B.thrD -= woff; B.thrN -= woff;
+    B.dbase = d;
   }
 }
 
@@ -591,9 +603,12 @@ __device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, cons
   int rem = 16, blk = 0;
   pk_reload<C>(B, gl, rem, P);
   while (__any_sync(FULL, B.active)) {
-    if (G == 1 && st != nullptr && ((++blk & 31) == 0)) {
-      pk_steal<C>(B, G, gl, d, *st);
-      if (!__any_sync(FULL, B.active)) break;
+    if ((++blk & 31) == 0) {
+      pk_rebase<C>(B, d, P);
+      if (G == 1 && st != nullptr) {
+        pk_steal<C>(B, G, gl, d, *st);
+        if (!__any_sync(FULL, B.active)) break;
+      }
     }
     pk_step<C>(B, G, gl, d, rem, P, level, esc, chc);
   }
@@ -806,8 +821,10 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
           return;
         }
       }
-    } else if ((blk & 31) == 0) {
-      pk_steal<C>(B, 1, gl, d, st);
+    }
+    if ((blk & 31) == 0) {
+      pk_rebase<C>(B, d, P);
+      if (t == 0) pk_steal<C>(B, 1, gl, d, st);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above
