@@ -73,8 +73,9 @@ class Aligner:
             B = N.Seqs(seqB.ctypes.data, offB.ctypes.data, offB.shape[0] - 1)
             pB = ctypes.byref(B)
         n = pairs.shape[0]
-        out = np.zeros(n, dtype=RESULT_DTYPE)
-        cells = np.zeros(n, dtype=np.int64) if want_cells else None
+        # every element is written by the call (on error the buffers are unspecified: include/xdrop.h)
+        out = np.empty(n, dtype=RESULT_DTYPE)
+        cells = np.empty(n, dtype=np.int64) if want_cells else None
         p = _params(M, mu, g, X, k)
         st = N.lib.xdrop_align_batch(self._h, ctypes.byref(A), pB, pairs.ctypes.data, n, ctypes.byref(p),
                                      out.ctypes.data, cells.ctypes.data if want_cells else None)

@@ -683,30 +683,39 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   if (rc) return rc;
   if (!A || !B || n_pairs < 0 || (n_pairs > 0 && (!pairs || !out))) return XDROP_EINVAL;
   if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
-  int64_t err = -1;
-  if ((rc = host_validate(A, err)) || (B != A && (rc = host_validate(B, err)))) {
-    ctx->err_index = err;
-    return rc;
+  // the read pools' H2D copy (the bulk of the call's host->device bytes) is issued first on the
+  // single-device path, so the host-side validation below runs while the DMA engine copies
+  // (pinned caller buffers); a validation error synchronises the stream before returning
+  const bool same = A == B || (A->seq == B->seq && A->offsets == B->offsets && A->n == B->n);
+  HostBatch hb{A, B, same, pairs, p, flags_of(ctx), out, cells_out};
+  const int m = (int)ctx->devs.size();
+  std::vector<DevSession> sess((size_t)m);
+  for (int g = 0; g < m; ++g) { sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; }
+  const bool single = m == 1 && ctx->opts.policy == XDROP_POLICY_CELLS;
+  auto pool_ok = [](const xdrop_seqs* S) {
+    return S && S->offsets && S->n >= 0 && (S->n == 0 || S->seq) && S->offsets[0] == 0 && S->offsets[S->n] >= 0;
+  };
+  if (single && pool_ok(A) && pool_ok(B)) {
+    if ((rc = sess[0].upload())) return rc;
   }
+  auto fail = [&](int r, int64_t e) {
+    if (single) cudaStreamSynchronize(ctx->devs[0].stream);
+    ctx->err_index = e;
+    return r;
+  };
+  int64_t err = -1;
+  if ((rc = host_validate(A, err)) || (B != A && (rc = host_validate(B, err)))) return fail(rc, err);
   // seeds and ids (a2), reported with the offending pair index
   for (int64_t t = 0; t < n_pairs; ++t) {
     const xdrop_pair& q = pairs[t];
     const int32_t bid = q.b_id & 0x7fffffff;   // bit 31 = XDROP_PAIR_RC
-    if (q.a_id < 0 || q.a_id >= A->n || bid >= B->n) { ctx->err_index = t; return XDROP_EINVAL; }
+    if (q.a_id < 0 || q.a_id >= A->n || bid >= B->n) return fail(XDROP_EINVAL, t);
     const int64_t la = A->offsets[q.a_id + 1] - A->offsets[q.a_id];
     const int64_t lb = B->offsets[bid + 1] - B->offsets[bid];
-    if (q.a_pos < 0 || q.b_pos < 0 || q.a_pos + (int64_t)p->k > la || q.b_pos + (int64_t)p->k > lb) {
-      ctx->err_index = t;
-      return XDROP_ESEED;
-    }
+    if (q.a_pos < 0 || q.b_pos < 0 || q.a_pos + (int64_t)p->k > la || q.b_pos + (int64_t)p->k > lb)
+      return fail(XDROP_ESEED, t);
   }
-  HostBatch hb{A, B, A == B || (A->seq == B->seq && A->offsets == B->offsets && A->n == B->n), pairs, p,
-               flags_of(ctx), out, cells_out};
-  const int m = (int)ctx->devs.size();
-  std::vector<DevSession> sess((size_t)m);
-  for (int g = 0; g < m; ++g) { sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; }
-
-  if (m == 1 && ctx->opts.policy == XDROP_POLICY_CELLS) {   // one device: no partition, no gather
+  if (single) {   // one device: no partition, no gather
     const auto t0 = std::chrono::steady_clock::now();
     rc = sess[0].run(nullptr, n_pairs);
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
