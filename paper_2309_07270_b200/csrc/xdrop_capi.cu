@@ -63,13 +63,16 @@ struct HostBuf {
 enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_P1, C_Q1T, C_Q1H, C_DONE1,                         // T1 record pool / queue
        C_P2, C_Q2T, C_Q2H,                                  // T2
-       C_P3, C_Q3T, C_HEAD3,                                // S = 1024 launch
+       C_P3, C_Q3T, C_HEAD3, C_DONE2,                       // S = 1024 (launch, or T3 of the shared kernel)
        C_P4, C_Q4T, C_HEAD4,                                // CTA launch (S = 4096)
        C_GEN, C_HEADG, C_HEADW,
        C_IDLE, C_SP, C_ST, C_SH, C_DONES,                   // tail stealing
        C_TLN,                                               // timeline records
        C_N };
 constexpr int kTimelineCap = 1 << 16;
+// S1024 checkpoints of the previous call above which the shared kernel (which resumes them as its
+// tier T3 while the other tiers drain, instead of in a launch after them) is chosen
+constexpr int64_t kSharedT3 = 256;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 32, HS_LVL = 48, HS_BYTES = 512 };
 
@@ -91,6 +94,7 @@ struct DevCtx {
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int64_t last_t1 = 0;      // T0 -> T1 checkpoints of the previous packed call (kernel choice)
+  int64_t last_t3 = 0;      // T2 -> S1024 checkpoints of the previous packed call (kernel choice)
   int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per call
   int age_us = 20;           // T1/T2 batch claims go partial once the oldest record waited this long (XDROP_AGE_US)
   int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
@@ -100,7 +104,7 @@ struct DevCtx {
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
       counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf;
-  xk::PkTier tier_host[3];          // staging of the shared packed kernel's tier descriptors (escbuf)
+  xk::PkTier tier_host[4];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -321,11 +325,12 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // the packed kernel reads its tier descriptors from device memory where used (rare paths)
       const xk::PkTier* tiers = nullptr;
       if (pk) {
-        CKR(D.escbuf.ensure(3 * sizeof(xk::PkTier)));
+        CKR(D.escbuf.ensure(4 * sizeof(xk::PkTier)));
         D.tier_host[0] = xk::PkTier{e1, e1, nullptr, nullptr, 0};                   // fresh (T0)
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
-        D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, nullptr, 1};               // T2 pool
-        CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 3 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
+        D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
+        D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)
+        CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 4 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
         tiers = D.escbuf.as<xk::PkTier>();
       }
       // packed kernel per call: the shared one when the previous call's escalated
@@ -333,7 +338,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       int shared = 0;
       if (pk) {
         const int64_t groups = (int64_t)D.sms * occ * 4 * (32 / XDROP_T1_G);
-        shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2) : (D.last_t1 >= 2 * groups);
+        shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2)
+                 : (D.last_t1 >= 2 * groups || D.last_t3 >= kSharedT3);
       }
       D.st.band_kernel = pk ? 1 + shared : 0;
       if (pk && shared && D.long_g == 2)
@@ -380,7 +386,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
     D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_P1];
     D.st.escalated[1] = hs[C_P2];
-    if (pk && !fl.force_wide && !fl.force_general) D.last_t1 = hs[C_P1];
+    if (pk && !fl.force_wide && !fl.force_general) { D.last_t1 = hs[C_P1]; D.last_t3 = hs[C_P3]; }
     D.st.escalated[2] = hs[C_P3];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];

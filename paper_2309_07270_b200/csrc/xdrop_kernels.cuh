@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
 pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  const PkTier* tiers, Steal st) {
   static_assert(GL * CL == 32, "4-lane units keep the lane window");
-  enum { NONE = 0, FRESH, T1, T2, STOLEN, LONG };
+  enum { NONE = 0, FRESH, T1, T2, T3, STOLEN, LONG };
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
@@ -944,12 +944,13 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
   bool idle = false;
   unsigned nap = 1000;
   for (;;) {
-    // lane 0 picks the unit: T2, T1, stolen, long, fresh (escalated work first)
+    // lane 0 picks the unit: T3, T2, T1, stolen, long, fresh (escalated work first)
     int kind = NONE, h = 0, k = 0, base = 0;
     if (lane == 0) {
       const bool t0_over = ld_volatile(c.head0) + first >= n_items;
-      h = claim_batch(c.q2_head, tiers[2].src, 32 / XDROP_T2_G, t0_over, c.age_us, k);
-      if (k) kind = T2;
+      h = claim(tiers[3].head, tiers[3].src.q_tail, 1, true, k);
+      if (k) kind = T3;
+      if (!kind) { h = claim_batch(c.q2_head, tiers[2].src, 32 / XDROP_T2_G, t0_over, c.age_us, k); if (k) kind = T2; }
       if (!kind) { h = claim_batch(c.q1_head, tiers[1].src, 32 / XDROP_T1_G, t0_over, c.age_us, k); if (k) kind = T1; }
       if (!kind) { h = claim(c.qs_head, st.es.q_tail, 32 / GL, true, k); if (k) kind = STOLEN; }
       if (!kind && t0ok && ld_volatile(c.head_long) < n_long) {
@@ -962,7 +963,11 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       }
       if (kind && idle) { atomicSub(c.idle, 1); idle = false; }
       if (!kind) {
-        if (merged_finished(c, n_items, tiers[1].src, tiers[2].src, st)) kind = -1;
+        // T2 done (=> T3's queue is final) and T3 drained, besides the lower tiers
+        const int t2 = ld_volatile(tiers[2].src.q_tail), t3 = ld_volatile(tiers[3].src.q_tail);
+        if (merged_finished(c, n_items, tiers[1].src, tiers[2].src, st) && ld_volatile(tiers[2].done) >= t2 &&
+            ld_volatile(tiers[3].head) >= t3)
+          kind = -1;
         else if (!idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
       } else {
         nap = 1000;
@@ -1004,10 +1009,12 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
         else atomicAdd(c.dones, k);
       }
     } else {
-      // T0 lane mode (G = 1), T1 (G = XDROP_T1_G) and T2 (G = XDROP_T2_G): one loop instance
-      const int t = kind == FRESH ? 0 : kind == T1 ? 1 : 2;
-      pk_unit<32>(P, t == 0 ? 1 : t == 1 ? XDROP_T1_G : XDROP_T2_G, t, tiers, items, base, n_items, h, k, st);
-      tl_rec(c, t == 0 ? 0 : t == 1 ? 3 : 4, t0);
+      // T0 lane mode (G = 1), T1 (G = XDROP_T1_G), T2 (G = XDROP_T2_G), T3 (G = 32, S = 1024): one
+      // loop instance
+      const int t = kind == FRESH ? 0 : kind == T1 ? 1 : kind == T2 ? 2 : 3;
+      pk_unit<32>(P, t == 0 ? 1 : t == 1 ? XDROP_T1_G : t == 2 ? XDROP_T2_G : 32, t, tiers, items, base, n_items,
+                  h, k, st);
+      tl_rec(c, t == 0 ? 0 : t == 1 ? 3 : t == 2 ? 4 : 6, t0);
       if (t == 0) {
         __threadfence();
         __syncwarp();

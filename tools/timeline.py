@@ -13,7 +13,7 @@ with xd.Aligner() as al:
     tl = al.timeline(); st = al.stats()
 t0 = tl[:, 2].min(); T = (tl[:, 3].max() - t0) / 1e6
 print(f"kernel span {T:.2f} ms, units {len(tl)}, stolen {st['stolen']}, band ms {st['level_ms'][0]:.2f}")
-names = ["lane", "long", "stolen", "pair", "warp", "endgame", "wide"]
+names = ["lane", "long", "stolen", "pair", "warp", "endgame", "t3"]
 for ty in range(7):
     m = tl[:, 0] == ty
     if m.any():
