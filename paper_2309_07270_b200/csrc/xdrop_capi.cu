@@ -68,6 +68,7 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_GEN, C_HEADG, C_HEADW,
        C_IDLE, C_SP, C_ST, C_SH, C_DONES,                   // tail stealing
        C_TLN,                                               // timeline records
+       C_ZERO,                                              // always 0 (an empty queue's tail)
        C_N };
 constexpr int kTimelineCap = 1 << 16;
 // S1024 checkpoints of the previous call above which the shared kernel (which resumes them as its
@@ -88,7 +89,10 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1;
+  int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
+  int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
+                              // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
@@ -169,6 +173,10 @@ int dev_open(DevCtx& D, int dev) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_gen, xk::general_kernel, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta, xk::band_cta_kernel<256, 16>, 256, 0));
   D.occ_cta = std::max(1, D.occ_cta);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta1k, xk::band_cta_kernel<128, 8>, 128, 0));
+  D.occ_cta1k = std::max(1, D.occ_cta1k);
+  if (const char* e = getenv("XDROP_SHARED_T3")) D.shared_t3 = atoi(e);
+  if (const char* e = getenv("XDROP_S1024")) D.s1024 = atoi(e);
   D.occ_l0 = std::max(1, D.occ_l0); D.occ_l1 = std::max(1, D.occ_l1);
   D.occ_l2 = std::max(1, D.occ_l2); D.occ_gen = std::max(1, D.occ_gen);
   CKR(D.h_small.ensure(HS_BYTES));
@@ -330,6 +338,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
         D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
         D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)
+        if (!D.shared_t3) D.tier_host[3].src.q_tail = ctr + C_ZERO;                  // T3 off: an empty queue
         CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 4 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
         tiers = D.escbuf.as<xk::PkTier>();
       }
@@ -339,7 +348,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       if (pk) {
         const int64_t groups = (int64_t)D.sms * occ * 4 * (32 / XDROP_T1_G);
         shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2)
-                 : (D.last_t1 >= 2 * groups || D.last_t3 >= kSharedT3);
+                 : (D.last_t1 >= 2 * groups || (D.shared_t3 && D.last_t3 >= kSharedT3));
       }
       D.st.band_kernel = pk ? 1 + shared : 0;
       if (pk && shared && D.long_g == 2)
@@ -366,7 +375,12 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
     } else {
-      if (pk)
+      // S1024 level: one warp with 32 cells per lane per extension (default), or one thread block of
+      // 4 warps x 32 lanes x 8 cells (XDROP_S1024=1: slower, its barrier per anti-diagonal costs more
+      // than the shorter per-lane work saves)
+      if (D.s1024)
+        xk::band_cta_kernel<128, 8><<<D.sms * D.occ_cta1k, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
+      else if (pk)
         xk::pk_resume_kernel<32, 32><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
       else
         xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);

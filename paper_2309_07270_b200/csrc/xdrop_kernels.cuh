@@ -1152,8 +1152,10 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
 // threads x CC cells = S cells (2S diagonals) in registers, the same cell update
 // as band_diag; neighbours across warp boundaries and the per-anti-diagonal
 // reductions go through shared memory, one barrier per anti-diagonal (buffers
-// double-buffered by anti-diagonal parity).  Resumes checkpoints of the S = 1024
-// warp level; an extension wider than S restarts in the unbounded kernel.
+// double-buffered by anti-diagonal parity).  <256, 16> (S = 4096) resumes the S = 1024 level's
+// checkpoints; an extension wider than that restarts in the unbounded kernel.  <128, 8> (S = 1024,
+// checkpointing into the <256, 16> queue) can replace the warp-per-extension S = 1024 level
+// (XDROP_S1024=1); measured slower.
 template <int NT, int CC>
 __global__ void __launch_bounds__(NT)
 band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
@@ -1306,8 +1308,28 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
       int dir = 0;
       if (qmx >= 2 * S - 2) dir = qmn >= 4 ? 1 : 2;
       else if (qmn <= 1) dir = qmx <= 2 * S - 5 ? -1 : 2;
-      if (dir == 2) {                              // wider than the block window: restart unbounded
-        if (t == 0) push_item(esc.fb_items, esc.fb_tail, item);
+      if (dir == 2) {
+        // wider than the block window: checkpoint for the next (wider) CTA level when `esc` has a
+        // record pool, else restart in the unbounded kernel
+        if (t == 0) s_q = esc.cap > 0 ? atomicAdd(esc.pool_tail, 1) : esc.cap;
+        __syncthreads();
+        const int slot = s_q;
+        if (slot < esc.cap) {
+          int* out = esc.pool + (size_t)slot * esc.rec_ints;
+          if (t == 0) {
+            out[0] = item; out[1] = d; out[2] = K0; out[3] = dbase; out[4] = thrW; out[5] = best;
+            out[6] = istar; out[7] = jstar; out[8] = minL1; out[9] = maxL1; out[10] = minL2; out[11] = maxL2;
+            out[12] = ia0; out[13] = jb0; out[14] = S;
+            out[15] = (int)(cells & 0xffffffffll); out[16] = (int)(cells >> 32); out[REC_T] = rec_stamp();
+          }
+#pragma unroll
+          for (int r = 0; r < NR; ++r) out[HDR + NR * t + r] = R[r];
+          __threadfence();
+          __syncthreads();
+          if (t == 0) push_item(esc.q, esc.q_tail, slot);
+        } else if (t == 0) {
+          push_item(esc.fb_items, esc.fb_tail, item);
+        }
         active = false;
         break;
       }

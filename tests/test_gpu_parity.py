@@ -79,10 +79,13 @@ def test_unrelated_wide_bands_escalate(xd):
     assert st["escalated"][0] > 0
 
 
-def test_cta_path_wide_band(xd):
+@pytest.mark.parametrize("s1024", ["0", "1"])
+def test_cta_path_wide_band(xd, s1024, monkeypatch):
     """X large enough that nothing is pruned, hull 1000-3000 cells: checkpoints travel
-    lane -> lane pair -> warp (256) -> warp (1024) -> CTA (4096) and resume exactly."""
+    lane -> lane pair -> warp (256) -> warp (1024; or a 4-warp CTA with XDROP_S1024=1) -> CTA (4096)
+    and resume exactly."""
     from synth import workload as W
+    monkeypatch.setenv("XDROP_S1024", s1024)
     w = W.random_pairs_workload(seed=9, n_pairs=8, len_lo=1200, len_hi=3000, k=5, X=100000, related=0.0)
     with xd.Aligner() as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=5, X=100000)
@@ -324,7 +327,8 @@ def test_packed_range_gate_and_negative_mismatch(xd, M, mu, g, X):
                                  {"XDROP_KERNEL": "1"}, {"XDROP_KERNEL": "2"},
                                  {"XDROP_KERNEL": "2", "XDROP_LONG_G": "2", "XDROP_LONG_ALPHA": "0.001"},
                                  {"XDROP_KERNEL": "2", "XDROP_OCC": "1", "XDROP_AGE_US": "0"},
-                                 {"XDROP_KERNEL": "2", "XDROP_STEAL_MIN": "16", "XDROP_LONG_G": "0"}])
+                                 {"XDROP_KERNEL": "2", "XDROP_STEAL_MIN": "16", "XDROP_LONG_G": "0"},
+                                 {"XDROP_KERNEL": "2", "XDROP_SHARED_T3": "0"}, {"XDROP_S1024": "1"}])
 def test_kernel_variants_identical(xd, env, monkeypatch):
     """32-bit vs packed T0, 1 block/SM, 1 T0 block/SM (the rest escalation-only), packed 2-lane long
     mode, the tiered and the shared packed kernels (the shared one also with 2-lane
@@ -341,12 +345,13 @@ def test_kernel_variants_identical(xd, env, monkeypatch):
     assert_same(res, cells, ref, rcells, f"variant {env}")
 
 
-@pytest.mark.parametrize("flags", [8, 16])
-def test_packed_resume_reaches_s1024(xd, flags):
+@pytest.mark.parametrize("flags,env", [(8, "0"), (16, "0"), (8, "1"), (16, "1")])
+def test_packed_resume_reaches_s1024(xd, flags, env, monkeypatch):
     """Unrelated continuations at X = 400 (packed path: X + M <= 510) outgrow T0 (32 cells), T1 (64
     tiered / 128 shared) and T2 (256): checkpoints resume in the packed 16-bit tiers up to the
     S = 1024 kernel, exactly, in both packed kernels."""
     from synth import workload as W
+    monkeypatch.setenv("XDROP_S1024", env)            # 1: the S = 1024 level as a 4-warp CTA
     w = W.random_pairs_workload(seed=660, n_pairs=24, len_lo=2500, len_hi=4000, k=11, X=400, related=0.0)
     with xd.Aligner(flags=flags) as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
