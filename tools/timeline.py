@@ -5,11 +5,14 @@ os.environ["XDROP_TIMELINE"] = "1"
 import numpy as np
 import paper_2309_07270_b200 as xd
 from synth import workload as W
-_nm = sys.argv[1] if len(sys.argv) > 1 else "ecoli"
+_nm, _, _x = (sys.argv[1] if len(sys.argv) > 1 else "ecoli").partition(":")
 w = W.config(_nm, scale=0.05) if _nm == "celegans" else W.config(_nm)
+if _x:
+    w = w.with_X(int(_x))
 with xd.Aligner() as al:
     for _ in range(2):
         r, c = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    print(al.stats()['band_kernel'], al.stats()['level_ms'])
     tl = al.timeline(); st = al.stats()
 t0 = tl[:, 2].min(); T = (tl[:, 3].max() - t0) / 1e6
 print(f"kernel span {T:.2f} ms, units {len(tl)}, stolen {st['stolen']}, band ms {st['level_ms'][0]:.2f}")
@@ -38,3 +41,11 @@ if len(sys.argv) > 2:
         for a in range(0, 16, 2):
             mm = (s >= a) & (s < a + 2)
             if mm.any(): print(f"  lane units starting [{a},{a+2}) ms: n={mm.sum()} dur mean {d[mm].mean():.2f} max {d[mm].max():.2f}")
+# start-up: units started and warps busy per 0.1 ms over the first 2.5 ms
+if os.environ.get("TL_START"):
+    for a in np.arange(0, 2.5, 0.1):
+        lo, hi = t0 + a * 1e6, t0 + (a + 0.1) * 1e6
+        st_n = ((tl[:, 2] >= lo) & (tl[:, 2] < hi))
+        busy = ((np.minimum(tl[:, 3], hi) - np.maximum(tl[:, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
+        kinds = np.bincount(tl[st_n, 0], minlength=7)
+        print(f"  [{a:4.1f},{a+0.1:4.1f}) started {st_n.sum():5d} by kind {kinds.tolist()} busy {busy*100:5.1f}%")
