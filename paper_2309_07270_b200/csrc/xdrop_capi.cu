@@ -69,6 +69,7 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_IDLE, C_SP, C_ST, C_SH, C_DONES,                   // tail stealing
        C_TLN,                                               // timeline records
        C_ZERO,                                              // always 0 (an empty queue's tail)
+       C_WP, C_WT, C_WH, C_WD,                              // endgame steals of the shared kernel
        C_N };
 constexpr int kTimelineCap = 1 << 16;
 // S1024 checkpoints of the previous call above which the shared kernel (which resumes them as its
@@ -107,8 +108,8 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf;
-  xk::PkTier tier_host[4];          // staging of the shared packed kernel's tier descriptors (escbuf)
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw;
+  xk::PkTier tier_host[5];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
   cudaEvent_t ev[12] = {};
@@ -188,7 +189,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -333,13 +334,21 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // the packed kernel reads its tier descriptors from device memory where used (rare paths)
       const xk::PkTier* tiers = nullptr;
       if (pk) {
-        CKR(D.escbuf.ensure(4 * sizeof(xk::PkTier)));
+        // endgame steals (T1/T2 extensions resumed 32 lanes x 8 cells once st.thresh warps idle): at
+        // most one record per resident pool group
+        const int capw = D.sms * occ * 4 * 8;
+        CKR(D.poolw.ensure((size_t)capw * rec3 * sizeof(int)));
+        CKR(D.qw.ensure((size_t)capw * sizeof(int)));
+        CK(cudaMemsetAsync(D.qw.p, 0xff, (size_t)capw * sizeof(int), s));
+        xk::Esc ew{D.poolw.as<int>(), rec3, capw, ctr + C_WP, D.qw.as<int>(), ctr + C_WT, gen, ctr + C_GEN};
+        CKR(D.escbuf.ensure(5 * sizeof(xk::PkTier)));
         D.tier_host[0] = xk::PkTier{e1, e1, nullptr, nullptr, 0};                   // fresh (T0)
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
         D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
         D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)
         if (!D.shared_t3) D.tier_host[3].src.q_tail = ctr + C_ZERO;                  // T3 off: an empty queue
-        CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 4 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
+        D.tier_host[4] = xk::PkTier{ew, e3, ctr + C_WH, ctr + C_WD, 1};             // endgame steals
+        CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 5 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
         tiers = D.escbuf.as<xk::PkTier>();
       }
       // packed kernel per call: the shared one when the previous call's escalated

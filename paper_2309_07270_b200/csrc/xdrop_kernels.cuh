@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
 pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  const PkTier* tiers, Steal st) {
   static_assert(GL * CL == 32, "4-lane units keep the lane window");
-  enum { NONE = 0, FRESH, T1, T2, T3, STOLEN, LONG };
+  enum { NONE = 0, FRESH, T1, T2, T3, STOLEN, LONG, WIDE };
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
@@ -948,8 +948,9 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
     int kind = NONE, h = 0, k = 0, base = 0;
     if (lane == 0) {
       const bool t0_over = ld_volatile(c.head0) + first >= n_items;
-      h = claim(tiers[3].head, tiers[3].src.q_tail, 1, true, k);
-      if (k) kind = T3;
+      h = claim(tiers[4].head, tiers[4].src.q_tail, 1, true, k);
+      if (k) kind = WIDE;
+      if (!kind) { h = claim(tiers[3].head, tiers[3].src.q_tail, 1, true, k); if (k) kind = T3; }
       if (!kind) { h = claim_batch(c.q2_head, tiers[2].src, 32 / XDROP_T2_G, t0_over, c.age_us, k); if (k) kind = T2; }
       if (!kind) { h = claim_batch(c.q1_head, tiers[1].src, 32 / XDROP_T1_G, t0_over, c.age_us, k); if (k) kind = T1; }
       if (!kind) { h = claim(c.qs_head, st.es.q_tail, 32 / GL, true, k); if (k) kind = STOLEN; }
@@ -963,10 +964,12 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       }
       if (kind && idle) { atomicSub(c.idle, 1); idle = false; }
       if (!kind) {
-        // T2 done (=> T3's queue is final) and T3 drained, besides the lower tiers
-        const int t2 = ld_volatile(tiers[2].src.q_tail), t3 = ld_volatile(tiers[3].src.q_tail);
+        // T2 done (=> T3's queue is final), the endgame steals done (they may push S1024 records) and
+        // T3 drained, besides the lower tiers
+        const int t2 = ld_volatile(tiers[2].src.q_tail), tw = ld_volatile(tiers[4].src.q_tail);
         if (merged_finished(c, n_items, tiers[1].src, tiers[2].src, st) && ld_volatile(tiers[2].done) >= t2 &&
-            ld_volatile(tiers[3].head) >= t3)
+            ld_volatile(tiers[4].done) >= tw && ld_volatile(tiers[4].head) >= tw &&
+            ld_volatile(tiers[3].head) >= ld_volatile(tiers[3].src.q_tail))
           kind = -1;
         else if (!idle && t0ok) { atomicAdd(c.idle, 1); idle = true; }
       } else {
@@ -985,7 +988,15 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
     k = __shfl_sync(FULL, k, 0);
     base = __shfl_sync(FULL, base, 0);
     const unsigned long long t0 = c.tl ? gtimer() : 0;
-    if (kind == STOLEN || kind == LONG) {
+    if (kind == WIDE) {
+      // endgame steal of a T1/T2 extension: one per warp, 32 lanes x 8 cells (S = 256), overflow to T3
+      const int slot = wait_entry_w(tiers[4].src.q, h, lane);
+      pk_resume<32, 8>(P, tiers[4].src.pool + (size_t)slot * tiers[4].src.rec_ints, 1, tiers[4].esc);
+      tl_rec(c, 7, t0);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(tiers[4].done, 1);
+    } else if (kind == STOLEN || kind == LONG) {
       // one GL x CL instance for both: fresh from the seed (long) or from a stolen record
       const int g = lane / GL, gl = lane % GL;
       Band16<CL> B;

@@ -580,7 +580,8 @@ __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int
 // tail stealing check (lane mode): once enough warps idle, checkpoint this lane's extension to
 // the steal queue if it still has >= min_rem anti-diagonals ahead
 template <int C>
-__device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st) {
+__device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st, const Esc& to) {
+  // (the group-uniform `left` test keeps pk_save's group shuffles converged for G > 1)
   int go = 0;
   if ((threadIdx.x & 31) == 0) go = ld_volatile(st.idle) >= st.thresh;
   go = __shfl_sync(FULL, go, 0);
@@ -588,7 +589,7 @@ __device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, con
     const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
     const int left = 2 * min(B.m - ic, B.n - (d - ic));
     if (left >= st.min_rem) {
-      pk_save<C>(B, G, gl, d, st.es);
+      pk_save<C>(B, G, gl, d, to);
       B.active = false;
     }
   }
@@ -606,7 +607,7 @@ __device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, cons
     if ((++blk & 31) == 0) {
       pk_rebase<C>(B, d, P);
       if (G == 1 && st != nullptr) {
-        pk_steal<C>(B, G, gl, d, *st);
+        pk_steal<C>(B, G, gl, d, *st, st->es);
         if (!__any_sync(FULL, B.active)) break;
       }
     }
@@ -824,7 +825,10 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
     }
     if ((blk & 31) == 0) {
       pk_rebase<C>(B, d, P);
-      if (t == 0) pk_steal<C>(B, 1, gl, d, st);
+      if (t == 0) pk_steal<C>(B, 1, gl, d, st, st.es);
+      // endgame: a T1/T2 extension with a long way to go leaves the wide C = 32 shape for the latency
+      // shape (32 lanes x 8 cells, tiers[4]) once enough warps idle
+      else if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[4].src);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above

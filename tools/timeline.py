@@ -16,8 +16,8 @@ with xd.Aligner() as al:
     tl = al.timeline(); st = al.stats()
 t0 = tl[:, 2].min(); T = (tl[:, 3].max() - t0) / 1e6
 print(f"kernel span {T:.2f} ms, units {len(tl)}, stolen {st['stolen']}, band ms {st['level_ms'][0]:.2f}")
-names = ["lane", "long", "stolen", "pair", "warp", "endgame", "t3"]
-for ty in range(7):
+names = ["lane", "long", "stolen", "pair", "warp", "endgame", "t3", "endsteal"]
+for ty in range(8):
     m = tl[:, 0] == ty
     if m.any():
         d = (tl[m, 3] - tl[m, 2]) / 1e6
@@ -47,5 +47,5 @@ if os.environ.get("TL_START"):
         lo, hi = t0 + a * 1e6, t0 + (a + 0.1) * 1e6
         st_n = ((tl[:, 2] >= lo) & (tl[:, 2] < hi))
         busy = ((np.minimum(tl[:, 3], hi) - np.maximum(tl[:, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
-        kinds = np.bincount(tl[st_n, 0], minlength=7)
+        kinds = np.bincount(tl[st_n, 0], minlength=8)
         print(f"  [{a:4.1f},{a+0.1:4.1f}) started {st_n.sum():5d} by kind {kinds.tolist()} busy {busy*100:5.1f}%")
