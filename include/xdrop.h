@@ -175,6 +175,8 @@ typedef struct {
   int64_t long_items;     /* extensions run in the multi-lane "long" mode of level 0 */
   int64_t stolen;         /* lane-mode extensions checkpointed at the tail and resumed 4 lanes wide */
   int64_t band_kernel;    /* band kernel of the call: 0 32-bit merged, 1 packed tiered, 2 packed shared */
+  int64_t cta_items;      /* extensions checkpointed into the S = 2048 thread-block level */
+  int64_t cta4k_items;    /* extensions checkpointed into the S = 4096 thread-block level */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 

@@ -64,7 +64,8 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_P1, C_Q1T, C_Q1H, C_DONE1,                         // T1 record pool / queue
        C_P2, C_Q2T, C_Q2H,                                  // T2
        C_P3, C_Q3T, C_HEAD3, C_DONE2,                       // S = 1024 (launch, or T3 of the shared kernel)
-       C_P4, C_Q4T, C_HEAD4,                                // CTA launch (S = 4096)
+       C_P4, C_Q4T, C_HEAD4,                                // CTA launch (S = 2048)
+       C_P5, C_Q5T, C_HEAD5,                                // CTA launch (S = 4096)
        C_GEN, C_HEADG, C_HEADW,
        C_IDLE, C_SP, C_ST, C_SH, C_DONES,                   // tail stealing
        C_TLN,                                               // timeline records
@@ -72,8 +73,11 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_WP, C_WT, C_WH, C_WD,                              // endgame steals of the shared kernel
        C_N };
 constexpr int kTimelineCap = 1 << 16;
-// S1024 checkpoints of the previous call above which the shared kernel (which resumes them as its
-// tier T3 while the other tiers drain, instead of in a launch after them) is chosen
+// Per-call choice of the packed kernel: the shared kernel once the previous call had
+// at least kSharedT1 T0 -> T1 checkpoints (escalated work is then a large or long-running part of
+// the batch: its T1/T2 pools and endgame steals beat the tiered kernel's per-tier loops) or at
+// least kSharedT3 S1024 checkpoints (it resumes them as tier T3 while the other tiers drain)
+constexpr int64_t kSharedT1 = 1024;
 constexpr int64_t kSharedT3 = 256;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 32, HS_LVL = 48, HS_BYTES = 512 };
@@ -90,7 +94,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
                               // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
@@ -108,7 +112,7 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw;
   xk::PkTier tier_host[5];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
@@ -175,6 +179,8 @@ int dev_open(DevCtx& D, int dev) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta, xk::band_cta_kernel<256, 16>, 256, 0));
   D.occ_cta = std::max(1, D.occ_cta);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta1k, xk::band_cta_kernel<128, 8>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta2k, xk::band_cta_kernel<128, 16>, 128, 0));
+  D.occ_cta2k = std::max(1, D.occ_cta2k);
   D.occ_cta1k = std::max(1, D.occ_cta1k);
   if (const char* e = getenv("XDROP_SHARED_T3")) D.shared_t3 = atoi(e);
   if (const char* e = getenv("XDROP_S1024")) D.s1024 = atoi(e);
@@ -189,7 +195,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -290,6 +296,10 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     const int64_t cap1 = n_items, cap2 = n_items;
     const int64_t cap3 = std::min<int64_t>(n_items, budget / ((xk::HDR + 2 * 256) * 4));
     const int64_t cap4 = std::min<int64_t>(n_items, budget / 8 / ((xk::HDR + 2 * 1024) * 4));
+    const int64_t cap5 = std::min<int64_t>(n_items, budget / 16 / ((xk::HDR + 2 * 2048) * 4));
+    const int rec5 = xk::HDR + 2 * 2048;
+    CKR(D.pool5.ensure((size_t)std::max<int64_t>(cap5, 1) * rec5 * sizeof(int)));
+    CKR(D.q5.ensure((size_t)std::max<int64_t>(cap5, 1) * sizeof(int)));
     const int rec1 = xk::HDR + 2 * 32, rec2 = xk::HDR + 2 * 128, rec3 = xk::HDR + 2 * 256, rec4 = xk::HDR + 2 * 1024;
     CKR(D.pool1.ensure((size_t)std::max<int64_t>(cap1, 1) * rec1 * sizeof(int)));
     CKR(D.pool2.ensure((size_t)std::max<int64_t>(cap2, 1) * rec2 * sizeof(int)));
@@ -308,6 +318,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::Esc e2{D.pool2.as<int>(), rec2, (int)cap2, ctr + C_P2, D.ovf2.as<int>(), ctr + C_Q2T, gen, ctr + C_GEN};
     xk::Esc e3{D.pool3.as<int>(), rec3, (int)cap3, ctr + C_P3, D.ovf3.as<int>(), ctr + C_Q3T, gen, ctr + C_GEN};
     xk::Esc e4{D.pool4.as<int>(), rec4, (int)cap4, ctr + C_P4, D.q4.as<int>(), ctr + C_Q4T, gen, ctr + C_GEN};
+    xk::Esc e5{D.pool5.as<int>(), rec5, (int)cap5, ctr + C_P5, D.q5.as<int>(), ctr + C_Q5T, gen, ctr + C_GEN};
     xk::Esc eg{nullptr, 0, 0, ctr + C_HEADW, nullptr, nullptr, gen, ctr + C_GEN};   // always falls back
     if (fl.force_general) {
       // everything goes to the unbounded kernel below
@@ -351,13 +362,13 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 5 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
         tiers = D.escbuf.as<xk::PkTier>();
       }
-      // packed kernel per call: the shared one when the previous call's escalated
-      // extensions alone could fill every resident T1 group twice over, else the tiered one
+      // packed kernel per call: the shared one when the previous call on this device
+      // checkpointed at least kSharedT1 extensions out of T0 (or kSharedT3 into S = 1024), else the
+      // tiered one (also for a context's first call)
       int shared = 0;
       if (pk) {
-        const int64_t groups = (int64_t)D.sms * occ * 4 * (32 / XDROP_T1_G);
         shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2)
-                 : (D.last_t1 >= 2 * groups || (D.shared_t3 && D.last_t3 >= kSharedT3));
+                 : (D.last_t1 >= kSharedT1 || (D.shared_t3 && D.last_t3 >= kSharedT3));
       }
       D.st.band_kernel = pk ? 1 + shared : 0;
       if (pk && shared && D.long_g == 2)
@@ -393,8 +404,11 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         xk::pk_resume_kernel<32, 32><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
       else
         xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
-      xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e4, ctr + C_HEAD4, eg, 2);
-      launches += 2;
+      // CTA levels: S = 2048 (4 warps x 32 lanes x 16 cells; twice the resident extensions of the
+      // 8-warp block) checkpointing its overflows for S = 4096 (8 warps x 32 x 16)
+      xk::band_cta_kernel<128, 16><<<D.sms * D.occ_cta2k, 128, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
+      xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e5, ctr + C_HEAD5, eg, 2);
+      launches += 3;
     }
     CK(cudaEventRecord(D.ev[10], s));
     CK(cudaGetLastError());
@@ -411,6 +425,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.escalated[1] = hs[C_P2];
     if (pk && !fl.force_wide && !fl.force_general) { D.last_t1 = hs[C_P1]; D.last_t3 = hs[C_P3]; }
     D.st.escalated[2] = hs[C_P3];
+    D.st.cta_items = hs[C_P4];
+    D.st.cta4k_items = hs[C_P5];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
     D.st.stolen = hs[C_SP];
