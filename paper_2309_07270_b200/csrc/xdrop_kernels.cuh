@@ -659,14 +659,25 @@ band_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 __device__ __forceinline__ int claim(int* head, const int* tail, int want, bool partial, int& k) {
   k = 0;
   int h = ld_volatile(head);
+  int t = ld_volatile(tail);
+  bool fresh = true;                    // t was read after h
   for (;;) {
-    const int t = ld_volatile(tail);
-    const int avail = t - h;
-    if (avail <= 0 || (avail < want && !partial)) return 0;
+    // the tail only grows, so a stale t under-estimates what is available: a failed CAS retries
+    // with it (one L2 round trip per attempt under contention, not two); re-read it only when it
+    // seems to leave nothing to claim
+    int avail = t - h;
+    if (avail <= 0 || (avail < want && !partial)) {
+      if (fresh) return 0;
+      t = ld_volatile(tail);
+      fresh = true;
+      avail = t - h;
+      if (avail <= 0 || (avail < want && !partial)) return 0;
+    }
     const int kk = min(want, avail);
     const int old = atomicCAS(head, h, h + kk);
     if (old == h) { k = kk; return h; }
     h = old;
+    fresh = false;
   }
 }
 // claim for a batch consumer: up to `want` entries, fewer only when `partial` or the oldest unclaimed
@@ -765,6 +776,9 @@ __device__ __forceinline__ void tl_rec(const MergedCtr& c, int type, unsigned lo
 #endif
 #ifndef XDROP_PK_MINBLOCKS
 #define XDROP_PK_MINBLOCKS 3
+#endif
+#ifndef XDROP_PK_C
+#define XDROP_PK_C 32          // cells per lane of the tiered kernel's packed lane mode (T0)
 #endif
 
 // the first t0_per_sm resident blocks of each SM take fresh (T0) extensions; the others serve
@@ -1139,7 +1153,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       busy();
       const unsigned long long t0 = c.tl ? gtimer() : 0;
       const int slot = base + lane;
-      pk_run<1, 32>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+      pk_run<1, XDROP_PK_C>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
       tl_rec(c, 0, t0);
       __threadfence();
       __syncwarp();
