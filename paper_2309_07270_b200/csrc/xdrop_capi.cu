@@ -100,6 +100,7 @@ struct DevCtx {
                               // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
   float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
+  int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int64_t last_t1 = 0;      // T0 -> T1 checkpoints of the previous packed call (kernel choice)
@@ -143,6 +144,7 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_LONG_G")) D.long_g = atoi(e);
   if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
   if (const char* e = getenv("XDROP_STEAL_MIN")) D.steal_min = atoi(e);
+  if (const char* e = getenv("XDROP_STEAL_DIV")) D.steal_div = std::max(1, atoi(e));
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
@@ -339,7 +341,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // >= 1024 anti-diagonals left (a full block pool falls back to the unbounded kernel)
       const int nwarps = D.sms * t0b * 4;
       xk::Esc es{D.pools.as<int>(), rec1, (int)caps, ctr + C_SP, D.qs.as<int>(), ctr + C_ST, gen, ctr + C_GEN};
-      xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / 8), D.steal_min, es};
+      xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / D.steal_div), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
       const unsigned grid = (unsigned)(D.sms * occ);
       // the packed kernel reads its tier descriptors from device memory where used (rare paths)
