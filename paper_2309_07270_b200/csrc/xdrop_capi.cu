@@ -355,7 +355,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         CK(cudaMemsetAsync(D.qw.p, 0xff, (size_t)capw * sizeof(int), s));
         xk::Esc ew{D.poolw.as<int>(), rec3, capw, ctr + C_WP, D.qw.as<int>(), ctr + C_WT, gen, ctr + C_GEN};
         CKR(D.escbuf.ensure(5 * sizeof(xk::PkTier)));
-        D.tier_host[0] = xk::PkTier{e1, e1, nullptr, nullptr, 0};                   // fresh (T0)
+        D.tier_host[0] = xk::PkTier{es, e1, nullptr, nullptr, 0};                   // fresh (T0; src: lane steals)
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
         D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
         D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)

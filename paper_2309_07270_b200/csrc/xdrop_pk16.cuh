@@ -282,7 +282,9 @@ __device__ __forceinline__ uint32_t pk_dead(const uint32_t (&ch)[C > 16 ? 2 : 1]
   }
 }
 
-template <int C, int PAR, bool CHECK>
+// REDUX: G = 32 groups reduce with CREDUX (one instruction each); the shared kernel's run-time-G
+// loop passes false so that its single instance carries no second reduction path (code size, I$)
+template <int C, int PAR, bool CHECK, bool REDUX = true>
 __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int qlo, int qhi, const Problem& P,
                                         const uint32_t (&chc)[C > 16 ? 2 : 1]) {
   uint32_t ch[C > 16 ? 2 : 1];
@@ -315,7 +317,7 @@ __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int 
     // 32-bit group key: value, then the lowest lane, then the lowest local cell (reading Q8:
     // smallest i); the live extents travel as one 16x2 word (tmax, 0x7FFF - tmin; -1 = none)
     int K = (int)((uint32_t)(kl >> 5) << 10) | ((31 - gl) << 5) | (kl & 31);
-    if (G == 32) {                                        // CREDUX: one instruction per reduction
+    if (REDUX && G == 32) {                               // CREDUX: one instruction per reduction
       K = __reduce_max_sync(FULL, K);
       tmin = __reduce_min_sync(FULL, lb ? tmin_l : EMIN);
       tmax = __reduce_max_sync(FULL, lb ? tmax_l : EMAX);
@@ -560,18 +562,18 @@ __device__ __forceinline__ void pk_chain_consts(const Band16<C>& B, uint32_t (&c
 }
 
 // two anti-diagonals (d+1, d+2) and the block end; boundary masking only when some group needs it
-template <int C>
+template <int C, bool REDUX = true>
 __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int& rem, const Problem& P, int level,
                                         const Esc& esc, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
   const int S = G * C;
   const int d2 = d + 2;
   const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
   if (__any_sync(FULL, need)) {
-    pk_diag<C, 1, true>(B, G, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
-    pk_diag<C, 0, true>(B, G, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
+    pk_diag<C, 1, true, REDUX>(B, G, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
+    pk_diag<C, 0, true, REDUX>(B, G, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
   } else {
-    pk_diag<C, 1, false>(B, G, gl, d + 1, 0, 0, P, chc);
-    pk_diag<C, 0, false>(B, G, gl, d2, 0, 0, P, chc);
+    pk_diag<C, 1, false, REDUX>(B, G, gl, d + 1, 0, 0, P, chc);
+    pk_diag<C, 0, false, REDUX>(B, G, gl, d2, 0, 0, P, chc);
   }
   d = d2;
   pk_block_end<C>(B, G, gl, d, rem, P, level, esc);
@@ -745,7 +747,7 @@ __device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int 
 // A tier of pk_merged_kernel's shared loop, read from device memory where used (rare paths), so
 // the queue descriptors take no registers in the loop.
 struct PkTier {
-  Esc src;          // records this tier resumes (pool tiers)
+  Esc src;          // records this tier resumes (pool tiers); tier 0: the lane-steal queue
   Esc esc;          // where its extensions that outgrow the window are checkpointed
   int* head;        // claim head of src's queue
   int* done;        // ended extensions of this tier (nullptr: not counted)
@@ -825,15 +827,15 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
     }
     if ((blk & 31) == 0) {
       pk_rebase<C>(B, d, P);
-      if (t == 0) pk_steal<C>(B, 1, gl, d, st, st.es);
-      // endgame: a T1/T2 extension with a long way to go leaves the wide C = 32 shape for the latency
-      // shape (32 lanes x 8 cells, tiers[4]) once enough warps idle
-      else if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[4].src);
+      // tail stealing: lane extensions to the 4-lane queue (tiers[0].src); endgame: a T1/T2 extension
+      // with a long way to go leaves the wide C = 32 shape for the latency shape (32 lanes x 8 cells,
+      // tiers[4].src) once enough warps idle.  One call site (pk_save is large)
+      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above
       return;
     }
-    pk_step<C>(B, G, gl, d, rem, P, tiers[t].level, tiers[t].esc, chc);
+    pk_step<C, true>(B, G, gl, d, rem, P, tiers[t].level, tiers[t].esc, chc);
   }
 }
