@@ -49,3 +49,9 @@ if os.environ.get("TL_START"):
         busy = ((np.minimum(tl[:, 3], hi) - np.maximum(tl[:, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
         kinds = np.bincount(tl[st_n, 0], minlength=8)
         print(f"  [{a:4.1f},{a+0.1:4.1f}) started {st_n.sum():5d} by kind {kinds.tolist()} busy {busy*100:5.1f}%")
+if os.environ.get("TL_START"):
+    for ty in range(8):
+        m = (tl[:, 0] == ty) & (tl[:, 2] - t0 < 2.5e6)
+        if m.any():
+            d = (tl[m, 3] - tl[m, 2]) / 1e6; e = (tl[m, 3] - t0) / 1e6
+            print(f"  first 2.5 ms {names[ty]:8s} n={m.sum():5d} dur p50 {np.median(d):.3f} max {d.max():.3f} ms; ends p50 {np.median(e):.3f} max {e.max():.3f} ms")
