@@ -1181,8 +1181,11 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
 // checkpoints; an extension wider than that restarts in the unbounded kernel.  <128, 8> (S = 1024,
 // checkpointing into the <256, 16> queue) can replace the warp-per-extension S = 1024 level
 // (XDROP_S1024=1); measured slower.
+#ifndef XDROP_CTA_MINB
+#define XDROP_CTA_MINB 3       // resident 4-warp CTA blocks per SM requested from ptxas
+#endif
 template <int NT, int CC>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, NT == 128 ? XDROP_CTA_MINB : 1)
 band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   constexpr int S = NT * CC, NR = 2 * CC, NW = NT / 32;
   constexpr int NCH = 4, CL = CC / NCH;
