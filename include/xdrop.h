@@ -177,6 +177,7 @@ typedef struct {
   int64_t band_kernel;    /* band kernel of the call: 0 32-bit merged, 1 packed tiered, 2 packed shared */
   int64_t cta_items;      /* extensions checkpointed into the S = 2048 thread-block level */
   int64_t cta4k_items;    /* extensions checkpointed into the S = 4096 thread-block level */
+  int64_t endgame_stolen; /* shared kernel: T1/T2 extensions moved to the 32 x 8 shape at the tail */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 

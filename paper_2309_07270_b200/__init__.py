@@ -146,7 +146,7 @@ class Aligner:
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
                     level_cells=list(s.level_cells), level_items=list(s.level_items),
                     long_items=s.long_items, stolen=s.stolen,
-                    band_kernel=("merged32", "tiered", "shared")[s.band_kernel], cta_items=s.cta_items, cta4k_items=s.cta4k_items)
+                    band_kernel=("merged32", "tiered", "shared")[s.band_kernel], cta_items=s.cta_items, cta4k_items=s.cta4k_items, endgame_stolen=s.endgame_stolen)
 
     def sched_stats(self) -> dict:
         s = N.SchedStats()

@@ -80,7 +80,8 @@ constexpr int kTimelineCap = 1 << 16;
 constexpr int64_t kSharedT1 = 1024;
 constexpr int64_t kSharedT3 = 256;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
-enum { HS_BAD = 32, HS_LVL = 48, HS_BYTES = 512 };
+enum { HS_BAD = 64, HS_LVL = 80, HS_BYTES = 512 };
+static_assert(C_N <= HS_BAD && HS_LVL + 16 <= HS_BYTES / 4, "host mirror layout: counters, bad flags, level sums");
 
 __global__ void init_counters_kernel(int* c, int n_items) {
   for (int i = threadIdx.x; i < C_N; i += blockDim.x) c[i] = (i == C_NITEMS) ? n_items : 0;
@@ -429,6 +430,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.escalated[2] = hs[C_P3];
     D.st.cta_items = hs[C_P4];
     D.st.cta4k_items = hs[C_P5];
+    D.st.endgame_stolen = hs[C_WP];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
     D.st.stolen = hs[C_SP];

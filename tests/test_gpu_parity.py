@@ -341,8 +341,13 @@ def test_kernel_variants_identical(xd, env, monkeypatch):
                                 related=0.7)
     with xd.Aligner() as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
     ref, rcells = oracle_of(w)
     assert_same(res, cells, ref, rcells, f"variant {env}")
+    if env.get("XDROP_KERNEL") == "2":
+        assert st["band_kernel"] == "shared"
+        if env.get("XDROP_STEAL_MIN") == "16":       # a small batch idles most warps at once
+            assert st["endgame_stolen"] > 0, st
 
 
 @pytest.mark.parametrize("flags,env", [(8, "0"), (16, "0"), (8, "1"), (16, "1")])
