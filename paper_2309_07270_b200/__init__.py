@@ -25,7 +25,10 @@ class Aligner:
     """A context over one or more GPUs (``xdrop_init``)."""
 
     def __init__(self, n_devices: int = 1, devices=None, policy: str = "cells", n_ranks: int = 1,
-                 batch_size: int = 10000, subbatches: int = 1, flags: int = 0):
+                 batch_size: int = 10000, subbatches: int = 1, flags: int = 0, kernel: str = "auto"):
+        """kernel: packed band kernel -- "auto" (per call from the previous call's escalations),
+        "tiered" or "shared" (XDROP_FLAG_TIERED / XDROP_FLAG_SHARED)."""
+        flags |= N.KERNELS[kernel]
         opts = N.InitOpts()
         self._dev_arr = None
         if devices is not None:

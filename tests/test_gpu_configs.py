@@ -52,17 +52,19 @@ def test_xsweep_full_size_sampled(xd):
     assert_same(res[idx], cells[idx], ref, rcells, "xsweep full sampled")
 
 
-@pytest.mark.parametrize("flags", [0, 8, 16])
-def test_celegans_shaped_small(xd, flags):
+@pytest.mark.parametrize("kernel", ["auto", "tiered", "shared"])
+def test_celegans_shaped_small(xd, kernel):
     """BASELINE configs[4] recipe (lognormal 2-40 kb, f_sp = 0.1) at 1/2000 scale, per-call kernel
     choice and both packed kernels forced."""
     from synth import workload as W
     w = W.make_pool_workload("celegans-small", 55, 600_000, 400, W._lognormal_len(8_000, 0.6, 2_000, 40_000),
                              8.0, 1_000, k=17, X=15, f_sp=0.1)
-    with xd.Aligner(flags=flags) as al:
+    with xd.Aligner(kernel=kernel) as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=15)
+        st = al.stats()
     ref, rcells = oracle_of(w)
-    assert_same(res, cells, ref, rcells, f"celegans small flags={flags}")
+    assert_same(res, cells, ref, rcells, f"celegans small kernel={kernel}")
+    assert st["band_kernel"] == ("tiered" if kernel == "auto" else kernel)   # auto: first call tiered
 
 
 def test_celegans_scaled_sample_shared_kernel_chosen(xd):
