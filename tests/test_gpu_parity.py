@@ -367,6 +367,20 @@ def test_packed_resume_reaches_s1024(xd, flags, env, monkeypatch):
     assert st["band_kernel"] == ("tiered" if flags == 8 else "shared")
 
 
+@pytest.mark.parametrize("kernel", ["tiered", "shared"])
+def test_packed_reaches_cta_levels(xd, kernel):
+    """Unrelated continuations at X = 500 (still the packed path) outgrow S = 1024: the packed
+    checkpoints resume in the 32-bit thread-block levels (S = 2048, then 4096), exactly."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=661, n_pairs=12, len_lo=6000, len_hi=8000, k=11, X=500, related=0.0)
+    with xd.Aligner(kernel=kernel) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
+    ref, rcells = oracle_of(w)
+    assert_same(res, cells, ref, rcells, f"packed -> CTA {kernel}")
+    assert st["band_kernel"] == kernel and st["cta_items"] > 0, st
+
+
 def test_random_scoring_sweep_packed_and_32bit(xd):
     """40 random (M, mu, g, X) settings across the API ranges, both sides of the packed-mode gate,
     ragged strand-mixed batches: every field bit-exact against the oracle."""
