@@ -81,7 +81,7 @@ constexpr int64_t kSharedT1 = 1024;
 constexpr int64_t kSharedT3 = 256;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 64, HS_LVL = 80, HS_BYTES = 512 };
-static_assert(C_N <= HS_BAD && HS_LVL + 16 <= HS_BYTES / 4, "host mirror layout: counters, bad flags, level sums");
+static_assert(int(C_N) <= int(HS_BAD) && HS_LVL + 16 <= HS_BYTES / 4, "host mirror layout: counters, bad flags, level sums");
 
 __global__ void init_counters_kernel(int* c, int n_items) {
   for (int i = threadIdx.x; i < C_N; i += blockDim.x) c[i] = (i == C_NITEMS) ? n_items : 0;
