@@ -74,3 +74,4 @@ def test_torchrun_reference_arm_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "GCUPS" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["ms_per_step"] > 0 and "sample_s" not in d["cpu_baseline"]
