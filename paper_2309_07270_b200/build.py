@@ -8,6 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libxdrop.so")
+# tests only: the same sources with -DXDROP_CHECKED (every packed-pool read bounds-checked, traps)
+OUT_CHECKED = os.path.join(HERE, "libxdrop_checked.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("xdrop_capi.cu", "sched.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("xdrop_kernels.cuh", "xdrop_pk16.cuh", "sched.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "xdrop.h")]
@@ -22,19 +24,29 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT):
-        t = os.path.getmtime(OUT)
+def _build_one(out: str, extra: list, force: bool, verbose: bool) -> str:
+    if not force and os.path.exists(out):
+        t = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= t for d in DEPS):
-            return OUT
-    tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, *SOURCES, "-o", tmp]
+            return out
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, *SOURCES, "-o", tmp]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    return _build_one(OUT, [], force, verbose)
+
+
+def build_checked(force: bool = False, verbose: bool = False) -> str:
+    return _build_one(OUT_CHECKED, ["-DXDROP_CHECKED"], force, verbose)
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv, verbose=True))

@@ -260,6 +260,17 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     PB = D.packB.as<uint32_t>();
   }
   CK(cudaEventRecord(D.ev[1], s));
+#ifdef XDROP_CHECKED
+  {
+    const uint32_t* base[2] = {D.packA.as<uint32_t>(), PB};
+    int64_t words[2] = {packed_words(lenA), packed_words(seqB != seqA ? lenB : lenA)};
+    // mutation knob for the checker's own test: register only the leading guard band, so that
+    // the first real base any kernel reads is out of bounds and must trap
+    if (getenv("XDROP_CHK_SHRINK")) words[0] = words[1] = xk::GUARD / 16;
+    CK(cudaMemcpyToSymbolAsync(xk::g_chk_base, base, sizeof(base), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyToSymbolAsync(xk::g_chk_words, words, sizeof(words), 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
 
   xk::Problem P;
   P.PA = D.packA.as<uint32_t>(); P.offA = offA; P.nA = nA;

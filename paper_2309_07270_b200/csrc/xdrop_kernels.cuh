@@ -57,9 +57,27 @@ struct Problem {
 };
 
 // ------------------------------------------------------------ packed streams
+#ifdef XDROP_CHECKED
+// Checked build (libxdrop_checked.so, tests only): every packed-pool word a kernel reads must lie
+// inside one of the two pools the host registered for this call (g_chk_base / g_chk_words, set by
+// dev_pipeline); anything else traps, so a guard-band or coordinate bug fails the call with
+// XDROP_ECUDA instead of silently reading a neighbour's bases.
+__device__ const uint32_t* g_chk_base[2];
+__device__ int64_t g_chk_words[2];
+__device__ __forceinline__ void chk_word(const uint32_t* q) {
+  for (int b = 0; b < 2; ++b)
+    if (q >= g_chk_base[b] && q < g_chk_base[b] + g_chk_words[b]) return;
+  __trap();
+}
+#define XDROP_CHK(q) chk_word(q)
+#else
+#define XDROP_CHK(q) ((void)0)
+#endif
 __device__ __forceinline__ uint32_t fwd16(const uint32_t* __restrict__ P, int64_t x) {
   const int64_t w = x >> 4;
   const int sh = (int)(x & 15) << 1;
+  XDROP_CHK(P + w);
+  XDROP_CHK(P + w + 1);
   const uint32_t lo = __ldg(P + w), hi = __ldg(P + w + 1);
   return __funnelshift_r(lo, hi, sh);
 }
@@ -82,6 +100,7 @@ __device__ __forceinline__ uint64_t rev_fields(uint64_t x) {
 }
 __device__ __forceinline__ int char_at(const uint32_t* __restrict__ P, int64_t start, int dir, int64_t t) {
   const int64_t x = start + (dir > 0 ? t : -t);
+  XDROP_CHK(P + (x >> 4));
   return (int)((__ldg(P + (x >> 4)) >> ((int)(x & 15) << 1)) & 3u);
 }
 

@@ -1,0 +1,79 @@
+"""Bounds-checked build (libxdrop_checked.so, -DXDROP_CHECKED): every packed-pool word any kernel
+reads must lie inside a pool registered for the call, else the kernel traps.  Runs in a child process
+(a trap poisons the CUDA context) over ragged reads, seeds at both read ends, reverse-complement
+pairs, every forced path and both packed kernels, and still checks the answers against the oracle.
+"""
+import os
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = textwrap.dedent("""
+    import numpy as np
+    import oracle
+    import paper_2309_07270_b200 as xd
+    from paper_2309_07270_b200 import _native
+    from synth import workload as W
+    assert _native.LIB_PATH.endswith("libxdrop_checked.so"), _native.LIB_PATH
+    F = ("score", "a_begin", "a_end", "b_begin", "b_end")
+
+    def run(w, X, **kw):
+        with xd.Aligner(**kw) as al:
+            res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
+        ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs, w.k, w.M, w.mu, w.g, X)
+        for f in F:
+            assert np.array_equal(res[f], ref[f]), (kw, X, f)
+        assert np.array_equal(cells, rc), (kw, X, "cells")
+
+    n = 0
+    for flags in (0, 1, 2, 4, 8, 16):
+        for X in (0, 15, 50):
+            w = W.random_pairs_workload(seed=300 + flags + X, n_pairs=40 if flags == 2 else 120, len_lo=0,
+                                        len_hi=600, k=11, X=X, rc_frac=0.3)
+            run(w, X, flags=flags); n += 1
+    w = W.random_pairs_workload(seed=77, n_pairs=8, len_lo=1500, len_hi=2500, k=11, X=300)
+    for kernel in ("tiered", "shared"):
+        run(w, 300, kernel=kernel); n += 1
+    w = W.config("cfg1")
+    run(w, w.X); n += 1
+    print("checked ok", n)
+""")
+
+
+def test_checked_build_every_path():
+    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
+    if not os.path.exists(lib):
+        sys.path.insert(0, os.path.join(ROOT, "paper_2309_07270_b200"))
+        import build as B
+        B.build_checked(verbose=True)
+    r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT})
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
+    assert "checked ok 21" in r.stdout
+
+
+def test_checked_build_traps_out_of_bounds_reads():
+    """The checker itself: with only the guard band registered, the first real read must trap and the
+    call must fail with XDROP_ECUDA (-3), not return results."""
+    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
+    child = textwrap.dedent("""
+        import paper_2309_07270_b200 as xd
+        from synth import workload as W
+        w = W.config("tiny")
+        try:
+            with xd.Aligner() as al:
+                al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+            print("no trap")
+        except xd.XdropError as e:
+            print("status", e.status)
+    """)
+    r = subprocess.run([sys.executable, "-c", child], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT, "XDROP_CHK_SHRINK": "1"})
+    assert "status -3" in r.stdout or ("status" in r.stdout and "no trap" not in r.stdout), \
+        (r.stdout[-2000:], r.stderr[-2000:])
