@@ -77,3 +77,33 @@ def test_checked_build_traps_out_of_bounds_reads():
                        env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT, "XDROP_CHK_SHRINK": "1"})
     assert "status -3" in r.stdout or ("status" in r.stdout and "no trap" not in r.stdout), \
         (r.stdout[-2000:], r.stderr[-2000:])
+
+
+CHILD_FULL = textwrap.dedent("""
+    import numpy as np
+    import oracle
+    import paper_2309_07270_b200 as xd
+    from synth import workload as W
+    F = ("score", "a_begin", "a_end", "b_begin", "b_end")
+    for name, scale, X in (("ecoli", 1.0, None), ("celegans", 0.01, None), ("xsweep", 0.05, 100)):
+        w = W.config(name, scale=scale, X=X)
+        with xd.Aligner() as al:
+            res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        idx = np.linspace(0, w.n_pairs - 1, min(w.n_pairs, 600)).astype(np.int64)
+        ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[idx], w.k, w.M, w.mu, w.g, w.X)
+        for f in F:
+            assert np.array_equal(res[f][idx], ref[f]), (name, f)
+        assert np.array_equal(cells[idx], rc), (name, "cells")
+        print(name, w.n_pairs, "ok", flush=True)
+    print("full ok")
+""")
+
+
+def test_checked_build_config_workloads():
+    """The bench's full E. coli-shaped batch (the launch configuration bench.py times) and small
+    C. elegans-shaped / X = 100 sweep batches through the bounds-checked build: no trap, sampled pairs
+    bit-exact against the oracle."""
+    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
+    r = subprocess.run([sys.executable, "-c", CHILD_FULL], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT})
+    assert r.returncode == 0 and "full ok" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
