@@ -70,8 +70,11 @@ __device__ __forceinline__ void chk_word(const uint32_t* q) {
   __trap();
 }
 #define XDROP_CHK(q) chk_word(q)
+// every extension result written must belong to an item of this call
+#define XDROP_CHK_ITEM(P, it) do { if ((it) < 0 || (int64_t)(it) >= 2 * (P).n_pairs) __trap(); } while (0)
 #else
 #define XDROP_CHK(q) ((void)0)
+#define XDROP_CHK_ITEM(P, it) ((void)0)
 #endif
 __device__ __forceinline__ uint32_t fwd16(const uint32_t* __restrict__ P, int64_t x) {
   const int64_t w = x >> 4;
@@ -469,6 +472,7 @@ __device__ __forceinline__ void band_block_end(Band<C>& B, int gl, int d, int& r
     if (gl == 0) {
       ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
       o.cells = B.cells; o.pad = 0;
+      XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
     }
     B.active = false;
@@ -591,6 +595,7 @@ __device__ __forceinline__ void band_run(const Problem& P, int item, int level, 
   if (B.active && B.m + B.n == 0) {
     if (gl == 0) {
       ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = level; o.cells = 1; o.pad = 0;
+      XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
     }
     B.active = false;
@@ -1344,6 +1349,7 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
       if ((e0 && e1) || d >= gm.m + gm.n) {
         if (t == 0) {
           ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level; o.cells = cells; o.pad = 0;
+          XDROP_CHK_ITEM(P, item);
           P.ext[item] = o;
         }
         active = false;
@@ -1477,6 +1483,7 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
     if (lane == 0) {
       ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level;
       o.cells = cells; o.pad = 0;
+      XDROP_CHK_ITEM(P, item);
       P.ext[item] = o;
     }
     __syncwarp();

@@ -487,6 +487,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
     if (gl == 0) {
       ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
       o.cells = B.cells; o.pad = 0;
+      XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
     }
     B.active = false;
@@ -655,6 +656,7 @@ __device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int it
   if (B.active && B.m + B.n == 0) {
     if (gl == 0) {
       ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = 0; o.cells = 1; o.pad = 0;
+      XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
     }
     B.active = false;
