@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded oracle sample")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the ncu child run that measures the dominant kernel's DRAM bytes per launch")
     return ap.parse_args()
 
 
@@ -156,13 +158,75 @@ class ClockSampler:
                 "samples": int(sm.size), "power_w_max": max(float(r[2]) for r in rows)}
 
 
+# ------------------------------------------------------------------- ncu traffic
+# ncu kernel-name regex of the dominant band kernel (stats()["band_kernel"])
+DOM_REGEX = {"tiered": "pk_tiered_kernel", "shared": "pk_merged_kernel", "merged32": "band_merged_kernel"}
+
+
+def ncu_traffic(args, kregex):
+    """DRAM bytes (read + write) of ONE launch of the dominant kernel, measured by ncu in a child run
+    of this same benchmark (same config; the launch profiled is the first timed step's, after the L2
+    flush).  Returns (bytes or None, note).  Numbers printed by the child are never used as bench values."""
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, "ncu not found"
+    warm = 3
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", f"regex:{kregex}", "--launch-skip", str(warm), "--launch-count", "1",
+           "--csv", sys.executable, os.path.abspath(__file__), "--steps", "1", "--warmup", str(warm),
+           "--no-e2e", "--no-cpu", "--no-traffic", "--config", args.config, "--scale", str(args.scale)]
+    if args.X is not None:
+        cmd += ["--X", str(args.X)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except Exception as e:          # noqa: BLE001
+        return None, f"ncu child failed: {type(e).__name__}"
+    vals = {}
+    import csv
+    import io
+    rows = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    for row in csv.reader(io.StringIO("\n".join(rows))):
+        if len(row) >= 3 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+            unit, val = row[-2], float(row[-1].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+                     "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1)
+            vals[row[-3]] = val * scale
+    if "dram__bytes_read.sum" not in vals:
+        return None, f"ncu gave no DRAM metrics (rc {r.returncode}): {(r.stdout + r.stderr)[-300:]!r}"
+    b = int(vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0))
+    return b, (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum on launch {warm + 1} of {kregex} "
+               f"(first timed step, after the L2 flush) in a child run of this config; "
+               f"read {int(vals['dram__bytes_read.sum'])} B, write {int(vals.get('dram__bytes_write.sum', 0))} B, "
+               f"{vals.get('gpu__time_duration.sum', 0):.3f} ms under ncu (not a bench value)")
+
+
 # ---------------------------------------------------------------------- cpu legs
+def cpu_info():
+    """Host CPU model, logical threads and physical cores (for the cpu_baseline / reference lines)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:
+        phys = None
+    return {"cpu_model": model, "logical_cpus": os.cpu_count() or 1, "physical_cores": phys}
+
+
 def oracle_sample(w, seconds: float, rng_seed: int = 0):
     """Bounded sample of the workload for the oracle: a pilot fixes the rate, then an
-    evenly spaced sample of pairs sized to ~`seconds` of CPU work is timed."""
+    evenly spaced sample of pairs sized to ~`seconds` of CPU work is timed.  Returns the
+    baseline dict and (idx, results, cells) of the sample (bench.py checks the GPU against them)."""
     import oracle
     n = w.n_pairs
-    cores = os.cpu_count() or 1
+    ci = cpu_info()
+    cores = ci["logical_cpus"]
     pilot = np.arange(0, n, max(1, n // 64))[:64]
     t = time.perf_counter()
     _, c = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[pilot], w.k, w.M, w.mu, w.g, w.X,
@@ -172,13 +236,18 @@ def oracle_sample(w, seconds: float, rng_seed: int = 0):
     m = int(min(n, max(pilot.size, seconds / per_pair)))
     idx = np.linspace(0, n - 1, m).astype(np.int64)
     t = time.perf_counter()
-    _, cells = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[idx], w.k, w.M, w.mu, w.g, w.X,
-                                  nthreads=cores)
+    res, cells = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[idx], w.k, w.M, w.mu, w.g, w.X,
+                                    nthreads=cores)
     dt = time.perf_counter() - t
-    return {"value": round(float(cells.sum()) / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+    mcells = float(cells.sum()) / dt / 1e6
+    base = {"value": round(mcells / 1e3, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
             "sample": f"{m} of {n} pairs (evenly spaced), {int(cells.sum())} cells in {dt:.2f} s "
                       f"on {cores} host threads; alignments/s {m / dt:.1f}",
+            "threads_used": cores, "cpu_model": ci["cpu_model"], "physical_cores": ci["physical_cores"],
+            "mcells_per_s_per_thread": round(mcells / cores, 2),
+            "mcells_per_s_per_physical_core": round(mcells / ci["physical_cores"], 2) if ci["physical_cores"] else None,
             "alignments_per_s": round(m / dt, 2), "sample_s": round(dt, 4), "sample_pairs": m}
+    return base, (idx, res, cells)
 
 
 def run_reference(args, world, rank):
@@ -187,20 +256,22 @@ def run_reference(args, world, rank):
         return
     w = shard_workload(args, 0)
     vals = []
+    t_run = time.perf_counter()
     for step in range(args.warmup + args.steps):
-        r = oracle_sample(w, seconds=max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup))))
+        r, _ = oracle_sample(w, seconds=max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup))))
         if step >= args.warmup:
             vals.append(r)
+    run_s = time.perf_counter() - t_run
     v = float(np.median([r["value"] for r in vals]))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GCUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": workload_desc(w, args, world),
-            # one step = the bounded sample; its wall time scaled to the whole batch of the config
-            "ms_per_step": round(float(np.median([r["sample_s"] * w.n_pairs / r["sample_pairs"] for r in vals]))
-                                 * 1e3, 3),
-            "ms_per_step_note": "median sample wall time x (pairs / sampled pairs): the oracle's time for the "
-                                "full batch, extrapolated when the sample is partial",
+            # one step = one bounded oracle sample of the workload (the time actually spent, not extrapolated)
+            "ms_per_step": round(float(np.median([r["sample_s"] for r in vals])) * 1e3, 3),
+            "ms_per_step_note": "measured wall time of one step = one bounded, evenly spaced oracle sample of the "
+                                "batch (sample size in cpu_baseline.sample); value = that sample's cells / time",
+            "run_s": round(run_s, 2),
             "cpu_baseline": {k: x for k, x in {**vals[-1], "value": v}.items()
                              if k not in ("sample_s", "sample_pairs")},
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -275,35 +346,42 @@ def run_native(args, world, rank, local):
                  "(merged into level 0)",
                  "xk::band_kernel<32,32> (warp/extension)", "xk::general_kernel"]
     achieved_ops = lvl_cells[dom] * ALGO_OPS_PER_CELL / (lvl_ms[dom] * 1e-3)
+    # algorithmic bytes of one band-kernel launch: the 2-bit pool read once
+    # (0.25 B/base) + per extension its queue entry (4 B), pair descriptor (16 B), two read offsets
+    # pairs (32 B) and its result record (32 B)
+    algo_bytes = int(w.offsets[-1]) // 4 + 2 * w.n_pairs * (4 + 16 + 32 + 32)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clocks = clk.summary()
     sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
-    # ALU pipe = 16 lanes/clk per SMSP x 4 SMSP x SMs x max clock
-    peak_ops = sms * 4 * 16 * sm_max * 1e6
+    # roofline denominators MEASURED on this device (csrc/xdrop_peaks.cu, single-instruction probes,
+    # SASS checked by tests/test_capi_host.py::test_peak_probes_sass): the T0 cells are packed 16-bit
+    # pairs, so the line's dtype (i16) peak is the VIMNMX3.S16x2 probe's lane-op rate x 2 16-bit ops;
+    # the int32 figure (VIMNMX3 probe) is kept beside it
+    pk = xd.alu_peaks(local)
+    p16 = 2.0 * pk["VIMNMX3.S16x2"]["lane_ops_per_s"]
+    p32 = pk["VIMNMX3"]["lane_ops_per_s"]
+    nominal32 = sms * 4 * 16 * sm_max * 1e6
     traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_band_kernel.json")))
-        traffic = prof.get("dram_bytes_per_launch")
-    except Exception:
-        pass
-    roofline = {"bound": "alu", "achieved": round(achieved_ops / 1e9, 1), "peak": round(peak_ops / 1e9, 1),
-                "unit": "Gop/s", "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
+    traffic_note = None
+    if not args.no_traffic and world == 1:
+        traffic, traffic_note = ncu_traffic(args, DOM_REGEX[band_kernel])
+    roofline = {"bound": "alu", "achieved": round(achieved_ops / 1e9, 1), "peak": round(p16 / 1e9, 1),
+                "unit": "Gop/s", "frac": round(achieved_ops / p16, 4), "traffic": traffic,
+                "peak_basis": "measured: 2 x the thread-instruction rate of the VIMNMX3.S16x2 probe "
+                              f"({pk['VIMNMX3.S16x2']['inst_per_clk_sm']:.1f} warp-inst/clk/SM) = 16-bit "
+                              "ALU-pipe ops/s (dtype i16: two cells per lane-op)",
+                "int32": {"peak": round(p32 / 1e9, 1), "frac": round(achieved_ops / p32, 4),
+                          "basis": f"measured VIMNMX3 (32-bit) probe, {pk['VIMNMX3']['inst_per_clk_sm']:.1f} "
+                                   "warp-inst/clk/SM"},
+                "nominal": {"int32_peak": round(nominal32 / 1e9, 1), "i16x2_peak": round(2 * nominal32 / 1e9, 1),
+                            "basis": f"{sms} SMs x 4 SMSP x 16 lanes/clk x {sm_max:.0f} MHz"},
+                "probes": {k: {"gops": round(v["lane_ops_per_s"] / 1e9, 1),
+                               "inst_per_clk_sm": round(v["inst_per_clk_sm"], 2)} for k, v in pk.items()},
                 "kernel": dom_names[dom], "kernel_ms": round(float(lvl_ms[dom]), 3),
                 "kernel_share_of_step": round(float(lvl_ms[dom]) / (total_ms / args.steps), 4),
                 "ops_per_cell": ALGO_OPS_PER_CELL, "cells_per_launch": int(lvl_cells[dom]),
-                "peak_basis": f"{sms} SMs x 4 SMSP x 16 INT32 lanes/clk (ALU pipe) x {sm_max:.0f} MHz",
-                # the T0 cell values are 16-bit pairs (VIMNMX/VIADDMNMX.S16x2: two cells per ALU lane-op),
-                # so the INT32 roofline of SURVEY §8(d) is not a hard ceiling; the 16x2 one is:
-                "simd16x2": {"peak": round(2 * peak_ops / 1e9, 1), "frac": round(achieved_ops / (2 * peak_ops), 4)}}
-    try:
-        p_alu, p_dual = al.int32_peak()
-        roofline["measured_int32_issue"] = {"alu_only_gops": round(p_alu / 1e9, 1),
-                                            "alu_plus_fma_gops": round(p_dual / 1e9, 1),
-                                            "note": "source-level int ops/s of int32_peak_kernel; ptxas routes ~40% "
-                                                    "of its adds to IMAD/VIADD on the FMA pipe, so this is an "
-                                                    "ALU+FMA rate, not a bound on the ALU pipe alone"}
-    except Exception:
-        pass
+                "algorithmic_bytes_per_launch": int(algo_bytes),
+                "traffic_note": traffic_note}
 
     # e2e through the host API (pinned host buffers)
     e2e = None
@@ -328,9 +406,26 @@ def run_native(args, world, rank, local):
         o = out_d.cpu().numpy()
         assert np.array_equal(o[:, 0], res_h["score"]) and np.array_equal(cells_h, cells_d.cpu().numpy())
 
+    # the oracle, as it stands, on a bounded sample (cpu_baseline) -- and the timed batch's results
+    # checked against it pair by pair (parity of the number this line reports)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = {k: x for k, x in oracle_sample(w, args.cpu_seconds).items() if k not in ("sample_s", "sample_pairs")}
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        base, (idx, ref, rcells) = oracle_sample(w, args.cpu_seconds if world == 1 else 2.0)
+        if world == 1:
+            cpu = {k: x for k, x in base.items() if k not in ("sample_s", "sample_pairs")}
+        o = out_d.cpu().numpy()[idx]
+        c = cells_d.cpu().numpy()[idx]
+        bad = np.zeros(idx.shape[0], dtype=bool)
+        for i, f in enumerate(("score", "a_begin", "a_end", "b_begin", "b_end")):
+            bad |= o[:, i] != ref[f]
+        bad |= c != rcells
+        parity = {"checked": int(idx.shape[0]), "mismatches": int(bad.sum()),
+                  "fields": "score, a_begin, a_end, b_begin, b_end, cells (bit-exact)",
+                  "sample": "the cpu_baseline oracle sample (evenly spaced pairs of the timed batch)"}
+        if bad.any():
+            print(f"PARITY FAILURE: {int(bad.sum())} of {idx.shape[0]} sampled pairs differ from the oracle",
+                  file=sys.stderr)
 
     if rank == 0:
         line = {"metric": METRIC,
@@ -342,7 +437,7 @@ def run_native(args, world, rank, local):
                 "data": "synthetic", "config": workload_desc(w, args, world),
                 "alignments_per_s": round(aps, 1), "cells_per_step": cells_all / args.steps,
                 "e2e": e2e, "gpu_launches": int(sum(s["launches"] for s in stats) * world),
-                "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+                "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "clocks": clocks,
                 "escalated_per_step": stats[-1]["escalated"][:3],
                 "level_ms": [round(float(x), 3) for x in lvl_ms], "step_ms_all": [round(x, 3) for x in step_ms]}
         emit(line, args)

@@ -134,7 +134,15 @@ int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
  * pool of nA reads with total length lenA (= offA[nA], passed so no D2H read
  * is needed); seqB may equal seqA.  Work is enqueued on `stream`
  * (cudaStream_t, NULL = the context's stream); the call returns after the
- * stream has completed so it can report validation errors. */
+ * stream has completed so it can report validation errors.
+ * Validation happens on the device (prep_kernel) before any extension runs: a
+ * pair whose read id is out of range, whose read's offsets leave the pool
+ * (off[r] < 0, off[r+1] < off[r] or off[r+1] > len), whose read exceeds
+ * XDROP_MAX_READ_LEN or whose seed leaves a read returns XDROP_ESEED with
+ * xdrop_last_error_index() = the smallest such pair index.  The work queue is
+ * emptied on the device first, so no band kernel dereferences an unvalidated
+ * id or position, and the context stays usable.  A base outside the alphabet
+ * returns XDROP_EALPHABET (checked first) with the pool base index. */
 int xdrop_align_batch_device(xdrop_ctx* ctx,
                              const char* seqA, const int64_t* offA, int64_t nA, int64_t lenA,
                              const char* seqB, const int64_t* offB, int64_t nB, int64_t lenB,
@@ -160,7 +168,8 @@ int xdrop_align_multiseed(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs*
                           const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
                           xdrop_result* out, int64_t* best, int64_t* cells_out);
 
-/* Counters of the last call on this context (first device). */
+/* Counters of the last call on this context: summed over every device and sub-batch turn of the
+ * call (the *_ms fields: the maximum over devices and turns). */
 typedef struct {
   int64_t items;          /* extensions (2 per pair) */
   int64_t escalated[4];   /* extensions that reached path level 1, 2, 3 (general) */
@@ -226,10 +235,15 @@ int xdrop_finalize(xdrop_ctx* ctx);
 const char* xdrop_strerror(int status);
 int64_t xdrop_last_error_index(const xdrop_ctx* ctx);
 
-/* Measure the INT32 issue rate of the first device (ops/s) with a dependent-
- * chain-free IADD3/LOP3/IMNMX/IMAD mix; fills ops_per_s[0] = ALU-pipe-only mix,
- * ops_per_s[1] = ALU+FMA-pipe mix.  Used only to cross-check the roofline. */
-int xdrop_int32_peak(xdrop_ctx* ctx, double* ops_per_s);
+/* Measured single-pipe integer issue rates of CUDA device `device` (the roofline denominators;
+ * SURVEY.md §8(d) P_int).  Six probes, each a loop of ONE SASS instruction kind in 8 independent
+ * chains per thread (csrc/xdrop_peaks.cu; tests/test_capi_host.py checks the SASS):
+ *   0 VIMNMX3.S16x2 (ALU pipe, two 16-bit lanes)  1 VIMNMX3 (ALU, 32-bit)  2 LOP3 (ALU)
+ *   3 IADD3 (ALU)  4 IMAD (FMA pipe)  5 VIMNMX3.S16x2 and IMAD alternating (both pipes).
+ * out[2p] = thread-instructions per second (CUDA events, best of 3), out[2p+1] = warp-instructions
+ * per SM per SM clock (clock64).  n_out >= 12, else XDROP_EINVAL.  Allocates and frees its own
+ * scratch; no context needed. */
+int xdrop_alu_peaks(int device, double* out, int n_out);
 
 #ifdef __cplusplus
 }

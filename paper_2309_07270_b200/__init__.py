@@ -14,7 +14,7 @@ from . import _native as N
 from ._native import RESULT_DTYPE, TRACE_DTYPE, XdropError  # noqa: F401
 
 __all__ = ["Aligner", "XdropError", "RESULT_DTYPE", "TRACE_DTYPE", "ring_left", "ring_right",
-           "sched_simulate"]
+           "sched_simulate", "alu_peaks"]
 
 
 def _params(M, mu, g, X, k):
@@ -41,6 +41,7 @@ class Aligner:
         h = ctypes.c_void_p()
         N.check(N.lib.xdrop_init(ctypes.byref(opts), ctypes.byref(h)), "xdrop_init")
         self._h = h
+        self._device0 = int(devices[0]) if devices is not None else 0   # device of align_device
 
     def close(self):
         if getattr(self, "_h", None):
@@ -91,14 +92,29 @@ class Aligner:
                      stream=None):
         """xdrop_align_batch_device on torch CUDA tensors (uint8 pool, int64 offsets,
         int32[n,4] pairs, int32[n,5] out, int64[n] cells or None)."""
+        if seqB is None:
+            seqB, offB = seqA, offA
+        n = int(pairs.shape[0]) if pairs.dim() == 2 else -1
+        _check_tensor("seqA", seqA, (1,), ("uint8", "int8"), self._device0)
+        _check_tensor("offA", offA, (1,), ("int64",), self._device0)
+        _check_tensor("seqB", seqB, (1,), ("uint8", "int8"), self._device0)
+        _check_tensor("offB", offB, (1,), ("int64",), self._device0)
+        _check_tensor("pairs", pairs, (2,), ("int32",), self._device0, cols=4)
+        _check_tensor("out", out, (2,), ("int32",), self._device0, rows=n, cols=5)
+        if cells is not None:
+            _check_tensor("cells", cells, (1,), ("int64",), self._device0, rows=n)
+        if offA.shape[0] < 1 or offB.shape[0] < 1:
+            raise ValueError("offsets need n+1 >= 1 entries")
         nA = offA.shape[0] - 1
         if lenA is None:
             lenA = int(seqA.shape[0])
-        if seqB is None:
-            seqB, offB, nB, lenB = seqA, offA, nA, lenA
+        if seqB is seqA and offB is offA:
+            nB, lenB = nA, lenA
         else:
             nB = offB.shape[0] - 1
             lenB = int(seqB.shape[0]) if lenB is None else lenB
+        if not (0 <= lenA <= seqA.shape[0] and 0 <= lenB <= seqB.shape[0]):
+            raise ValueError("lenA / lenB exceed the pool tensors")
         p = _params(M, mu, g, X, k)
         s = stream.cuda_stream if stream is not None else None
         st = N.lib.xdrop_align_batch_device(
@@ -177,10 +193,36 @@ class Aligner:
         out[:, 2:] = buf[:, 1:].astype(np.int64)
         return out
 
-    def int32_peak(self):
-        out = np.zeros(2, dtype=np.float64)
-        N.check(N.lib.xdrop_int32_peak(self._h, out.ctypes.data), "xdrop_int32_peak")
-        return float(out[0]), float(out[1])
+
+
+PEAK_PROBES = ("VIMNMX3.S16x2", "VIMNMX3", "LOP3", "IADD3", "IMAD", "VIMNMX3.S16x2+IMAD")
+
+
+def alu_peaks(device: int = 0) -> dict:
+    """xdrop_alu_peaks: measured issue rate of each single-instruction probe on `device` ->
+    {probe: {"lane_ops_per_s": .., "inst_per_clk_sm": ..}} (csrc/xdrop_peaks.cu)."""
+    out = np.zeros(2 * len(PEAK_PROBES), dtype=np.float64)
+    st = N.lib.xdrop_alu_peaks(int(device), out.ctypes.data, out.shape[0])
+    N.check(st, "xdrop_alu_peaks")
+    return {p: {"lane_ops_per_s": float(out[2 * i]), "inst_per_clk_sm": float(out[2 * i + 1])}
+            for i, p in enumerate(PEAK_PROBES)}
+
+
+def _check_tensor(name, t, dims, dtypes, device, rows=None, cols=None):
+    """Marshalling guard of align_device: the C ABI reads raw device pointers with fixed layouts
+    (include/xdrop.h), so a wrong dtype, shape, stride or device would be misread silently."""
+    if t.dim() not in dims:
+        raise ValueError(f"{name}: expected {dims[0]}-D tensor, got shape {tuple(t.shape)}")
+    if str(t.dtype).replace("torch.", "") not in dtypes:
+        raise ValueError(f"{name}: expected dtype {dtypes[0]}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: tensor must be contiguous")
+    if t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name}: expected a tensor on cuda:{device}, got {t.device}")
+    if rows is not None and t.shape[0] != rows:
+        raise ValueError(f"{name}: expected {rows} rows, got {t.shape[0]}")
+    if cols is not None and (t.dim() != 2 or t.shape[1] != cols):
+        raise ValueError(f"{name}: expected {cols} columns, got shape {tuple(t.shape)}")
 
 
 def ring_left(rank: int, batch: int, counts) -> int | None:

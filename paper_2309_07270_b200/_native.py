@@ -66,7 +66,7 @@ EXPORTS = [
     "xdrop_init", "xdrop_align_batch", "xdrop_align_batch_device", "xdrop_last_stats",
     "xdrop_best_seed_device", "xdrop_align_multiseed",
     "xdrop_last_sched_stats", "xdrop_last_trace", "xdrop_sched_simulate", "xdrop_ring_left",
-    "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_int32_peak",
+    "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_alu_peaks",
     "xdrop_last_timeline",
 ]
 
@@ -100,7 +100,7 @@ def _load():
     lib.xdrop_strerror.restype = ctypes.c_char_p
     lib.xdrop_last_error_index.argtypes = [P]
     lib.xdrop_last_error_index.restype = ctypes.c_int64
-    lib.xdrop_int32_peak.argtypes = [P, P]
+    lib.xdrop_alu_peaks.argtypes = [ctypes.c_int, P, ctypes.c_int]
     lib.xdrop_last_timeline.argtypes = [P, P, ctypes.c_int64]
     lib.xdrop_last_timeline.restype = ctypes.c_int64
     return lib

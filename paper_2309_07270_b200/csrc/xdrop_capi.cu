@@ -275,6 +275,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   xk::Problem P;
   P.PA = D.packA.as<uint32_t>(); P.offA = offA; P.nA = nA;
   P.PB = PB; P.offB = offB; P.nB = nB;
+  P.lenA = lenA; P.lenB = lenB;
   P.pairs = pairs; P.n_pairs = n_pairs;
   P.M = p.match; P.mu = p.mismatch; P.g = p.gap; P.X = p.xdrop; P.k = p.k;
   P.keym = 1 << xk::KEYSH;
@@ -292,7 +293,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
         P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
     xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
-                                       (long long)D.sms * t0b * 128, D.long_g ? D.long_alpha : 0.f);
+                                       (long long)D.sms * t0b * 128, D.long_g ? D.long_alpha : 0.f,
+                                       D.bad.as<unsigned long long>() + 1, ctr + C_NITEMS);
     xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
         D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
     launches += 3;
@@ -641,11 +643,26 @@ struct HostBatch {
 
 // Run a subset of pairs (indices idx) on device D; pools are uploaded once per
 // call per device (upload_pools), pairs/results per sub-batch.
+// accumulate the counters of one pipeline run into a call's totals: counts add up, times take the
+// maximum (devices run concurrently), the kernel choice is the last one
+void stats_add(xdrop_stats& a, const xdrop_stats& b) {
+  a.items += b.items; a.cells += b.cells; a.launches += b.launches;
+  for (int l = 0; l < 4; ++l) {
+    a.escalated[l] += b.escalated[l]; a.level_cells[l] += b.level_cells[l]; a.level_items[l] += b.level_items[l];
+    a.level_ms[l] = std::max(a.level_ms[l], b.level_ms[l]);
+  }
+  a.kernel_ms = std::max(a.kernel_ms, b.kernel_ms); a.total_ms = std::max(a.total_ms, b.total_ms);
+  a.pack_ms = std::max(a.pack_ms, b.pack_ms);
+  a.long_items += b.long_items; a.stolen += b.stolen; a.band_kernel = b.band_kernel;
+  a.cta_items += b.cta_items; a.cta4k_items += b.cta4k_items; a.endgame_stolen += b.endgame_stolen;
+}
+
 struct DevSession {
   DevCtx* D;
   const HostBatch* hb;
   bool uploaded = false;
   bool packed = false;
+  xdrop_stats acc{};          // this device's counters summed over the call's turns
   int upload() {
     if (uploaded) return 0;
     DevCtx& d = *D;
@@ -694,6 +711,7 @@ struct DevSession {
                           d.pairs.as<PairDesc>(), n, *hb->p, d.out5.as<int>(), d.cells.as<long long>(),
                           d.stream, hb->fl, !packed);
     if (rc == 0 || rc != XDROP_EALPHABET) packed = true;
+    if (rc == 0) stats_add(acc, d.st);
     if (rc) {
       if (d.err_index >= 0 && rc != XDROP_EALPHABET && idx) d.err_index = idx[d.err_index];
       return rc;
@@ -811,8 +829,9 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   rc = xdrop_sched_run(cfg, w.data(), n_pairs, runner, &ctx->sched, &ctx->trace);
   if (!rc) rc = first_rc;
   if (rc) { ctx->err_index = first_err; return rc; }
-  // stats: sum over devices of the last pipeline runs (per-call granularity for 1 device)
-  ctx->st = ctx->devs[0].st;
+  // stats: every device's turns of this call, summed (times: the maximum over devices and turns)
+  ctx->st = xdrop_stats{};
+  for (auto& se : sess) stats_add(ctx->st, se.acc);
   return 0;
 }
 
@@ -839,32 +858,6 @@ extern "C" int64_t xdrop_last_trace(const xdrop_ctx* ctx, xdrop_trace_event* buf
   const int64_t n = (int64_t)ctx->trace.size();
   for (int64_t t = 0; t < n && t < cap && buf; ++t) buf[t] = ctx->trace[(size_t)t];
   return n;
-}
-
-// -------------------------------------------------------- INT32 peak probe
-extern "C" int xdrop_int32_peak(xdrop_ctx* ctx, double* ops_per_s) {
-  if (!ctx || !ctx->alive || !ops_per_s) return XDROP_EINVAL;
-  DevCtx& D = ctx->devs[0];
-  CK(cudaSetDevice(D.dev));
-  CKR(D.bad.ensure(16));
-  const int iters = 4096, threads = 256, blocks = D.sms * 8;
-  for (int mode = 0; mode < 2; ++mode) {
-    float best = 1e30f;
-    for (int rep = 0; rep < 4; ++rep) {
-      CK(cudaEventRecord(D.ev[5], D.stream));
-      if (mode == 0) xk::int32_peak_kernel<false><<<blocks, threads, 0, D.stream>>>(iters, rep, D.bad.as<int>());
-      else xk::int32_peak_kernel<true><<<blocks, threads, 0, D.stream>>>(iters, rep, D.bad.as<int>());
-      CK(cudaEventRecord(D.ev[6], D.stream));
-      CK(cudaEventSynchronize(D.ev[6]));
-      float ms = 0;
-      cudaEventElapsedTime(&ms, D.ev[5], D.ev[6]);
-      if (rep > 0) best = std::min(best, ms);
-    }
-    // ops per inner body: 16 unrolled x (4 a-chains x 2 ops + 4 b-chains x 2 ops) = 256
-    const double ops = (double)blocks * threads * iters * 16.0 * 16.0;
-    ops_per_s[mode] = ops / (best * 1e-3);
-  }
-  return 0;
 }
 
 // f4 host form: the batch, then the selection kernel on the first device

@@ -49,6 +49,7 @@ struct PairDesc { int32_t a_id, b_id, a_pos, b_pos; };
 struct Problem {
   const uint32_t* PA; const int64_t* offA; int64_t nA;
   const uint32_t* PB; const int64_t* offB; int64_t nB;
+  int64_t lenA, lenB;  // bases in each pool (prep_kernel checks every read's offsets against them)
   const PairDesc* pairs; int64_t n_pairs;
   int M, mu, g, X, k;
   int keym;          // 128: argmax key multiplier, passed at run time so ptxas keeps it an IMAD (FMA pipe)
@@ -60,8 +61,10 @@ struct Problem {
 #ifdef XDROP_CHECKED
 // Checked build (libxdrop_checked.so, tests only): every packed-pool word a kernel reads must lie
 // inside one of the two pools the host registered for this call (g_chk_base / g_chk_words, set by
-// dev_pipeline); anything else traps, so a guard-band or coordinate bug fails the call with
-// XDROP_ECUDA instead of silently reading a neighbour's bases.
+// dev_pipeline); anything else traps, so a guard-band or coordinate bug that leaves the pools fails
+// the call with XDROP_ECUDA.  The check is against POOL bounds: a coordinate bug that reads another
+// read of the same pool is caught by the oracle parity of the tests, not here.  The bounds are
+// per-module device globals, so the checked build supports one context per device at a time.
 __device__ const uint32_t* g_chk_base[2];
 __device__ int64_t g_chk_words[2];
 __device__ __forceinline__ void chk_word(const uint32_t* q) {
@@ -1520,18 +1523,27 @@ __global__ void pack_kernel(const char* __restrict__ seq, int64_t len, uint32_t*
   out[w] = word;
 }
 
-// validate pairs, estimate costs, histogram of cost buckets
+// validate pairs, estimate costs, histogram of cost buckets.  A pair is valid when its read ids are
+// in range, both reads' offsets lie inside their pool (0 <= off[r] <= off[r+1] <= len), both reads
+// are at most max_len bases and the seed lies inside both reads (include/xdrop.h, XDROP_ESEED).
+// An invalid pair sets *bad_pair to (the minimum of) its index; scan_kernel then empties the
+// queue, so no band kernel ever dereferences an unvalidated id or position (device API).
+__device__ __forceinline__ bool read_ok(const int64_t* off, int64_t n, int64_t len, int64_t r, int64_t& L) {
+  if (r < 0 || r >= n) return false;
+  const int64_t o0 = off[r], o1 = off[r + 1];
+  L = o1 - o0;
+  return o0 >= 0 && o1 >= o0 && o1 <= len;
+}
 __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict__ hist,
                             unsigned long long* bad_pair, int max_len) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P.n_pairs) return;
   const PairDesc pd = P.pairs[p];
   const int bid = pd.b_id & 0x7fffffff;
-  bool ok = pd.a_id >= 0 && pd.a_id < P.nA && bid < P.nB;
+  int64_t lenA = 0, lenB = 0;
+  bool ok = read_ok(P.offA, P.nA, P.lenA, pd.a_id, lenA) && read_ok(P.offB, P.nB, P.lenB, bid, lenB);
   int wl = 0, wr = 0;
   if (ok) {
-    const int64_t lenA = P.offA[pd.a_id + 1] - P.offA[pd.a_id];
-    const int64_t lenB = P.offB[bid + 1] - P.offB[bid];
     ok = pd.a_pos >= 0 && pd.b_pos >= 0 && pd.a_pos + (int64_t)P.k <= lenA &&
          pd.b_pos + (int64_t)P.k <= lenB && lenA <= max_len && lenB <= max_len;
     if (ok) {
@@ -1552,7 +1564,8 @@ __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict_
 // a sizeable fraction of the whole launch's per-lane work -- form the prefix
 // [0, n_long) of the sorted queue (alpha <= 0 disables the long mode).
 __global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ cursor, int* __restrict__ n_long,
-                            long long lanes, float alpha) {
+                            long long lanes, float alpha, const unsigned long long* __restrict__ bad_pair,
+                            int* __restrict__ n_items) {
   __shared__ int part[1024];
   __shared__ unsigned long long wsum[32];
   constexpr int PER = NBUCKET / 1024;
@@ -1591,6 +1604,9 @@ __global__ void scan_kernel(const int* __restrict__ hist, int* __restrict__ curs
       if (tb < NBUCKET) nl = cursor[tb] + hist[tb];   // items in buckets >= tb
     }
     *n_long = nl;
+    // a pair failed validation (prep_kernel): no extension is queued, every band kernel finds an
+    // empty queue (the force-general path reads the same count), and the host returns XDROP_ESEED
+    if (*bad_pair != ~0ull) { *n_items = 0; *n_long = 0; }
   }
 }
 
@@ -1647,7 +1663,6 @@ __global__ void combine_kernel(Problem P, int* __restrict__ out5, long long* __r
   }
 }
 
-// ----------------------------------------------------- INT32 issue-rate probe
 // f4: best seed per candidate (adjacent rows with equal a_id, b_id); the thread of a candidate's
 // first row scans the run once (O(n) total), ties to the lowest row
 __global__ void best_seed_kernel(const PairDesc* __restrict__ pairs, const int* __restrict__ res5, int64_t n,
@@ -1669,21 +1684,6 @@ __global__ void best_seed_kernel(const PairDesc* __restrict__ pairs, const int* 
     if (s > bs) { bs = s; bi = j; }
   }
   for (int64_t t = i; t <= j; ++t) best[t] = bi;
-}
-
-template <bool DUAL>
-__global__ void int32_peak_kernel(int iters, int seed, int* sink) {
-  int a0 = threadIdx.x + seed, a1 = a0 ^ 0x55, a2 = a0 * 3, a3 = a0 + 7;
-  int b0 = a0 ^ 0x1234, b1 = a1 + 11, b2 = a2 ^ 0x777, b3 = a3 * 5;
-  for (int it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      a0 = max(a0 + b1, a2); a1 = (a1 ^ b0) + a3; a2 = max(a2, b2) - a0; a3 = a3 + (b3 ^ a1);
-      if (DUAL) { b0 = b0 * 3 + a1; b1 = b1 * 5 + a2; b2 = b2 * 7 + a3; b3 = b3 * 9 + a0; }
-      else { b0 = max(b0, a1) ^ 3; b1 = (b1 ^ a2) + 5; b2 = min(b2, a3) + 7; b3 = (b3 + a0) ^ 9; }
-    }
-  }
-  if ((a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3) == 0x7fffffff) *sink = 1;
 }
 
 }  // namespace xk

@@ -20,6 +20,7 @@ ring order, one2all global serialisation) using the trace alone.
 """
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -129,7 +130,9 @@ class RankResult:
 def run_rank(rank: int, n_ranks: int, policy: str, m: int, n_pairs: int, batch_size: int, c: int,
              comm, runner, clock=time.monotonic) -> RankResult:
     """One rank's whole schedule.  runner(gpu_slots, idx) aligns pairs idx on the given
-    device slots (all m for one2all, rank mod m otherwise) and returns when done."""
+    device slots (all m for one2all, rank mod m otherwise) and returns when done; it may return
+    {slot: (t0, t1)} with each device's own busy interval (one2all runs its devices concurrently),
+    else every slot's turn spans the whole call."""
     if policy not in POLICIES:
         raise ValueError(policy)
     lo, hi = rank_chunk(n_pairs, n_ranks, rank)
@@ -162,11 +165,11 @@ def run_rank(rank: int, n_ranks: int, policy: str, m: int, n_pairs: int, batch_s
             for s_i, idx in enumerate(subs):
                 sub_no = (s_i + 1) if opt else it
                 t0 = clock()
-                if idx.size:
-                    runner(slots, idx)
+                per = runner(slots, idx) if idx.size else None
                 t1 = clock()
                 for g in slots:
-                    res.turns.append(Turn(rank, g, b, sub_no, int(idx.size), t0, t1))
+                    g0, g1 = per[g] if per and g in per else (t0, t1)
+                    res.turns.append(Turn(rank, g, b, sub_no, int(idx.size), g0, g1))
             nx = ring.next(u, b, it)
             if nx >= 0 and nx != u:
                 comm.send(members[nx], 1)                                # l.26-30
@@ -268,18 +271,41 @@ def _worker(rank, n_ranks, port, policy, m, batch_size, c, w_arrays, params, use
         res_off = {g: torch.from_numpy(off).to(devs[g]) for g in slots}
         dpairs = {g: torch.from_numpy(pairs).to(devs[g]) for g in slots}
 
+        def run_part(g, part, times):
+            t0 = time.monotonic()
+            dev = devs[g]
+            sub = dpairs[g][torch.from_numpy(part).to(dev)]
+            o = torch.zeros((part.size, 5), dtype=torch.int32, device=dev)
+            cl = torch.zeros(part.size, dtype=torch.int64, device=dev)
+            als[g].align_device(res_seq[g], res_off[g], sub, o, cl, **params)   # ctypes drops the GIL
+            out[part] = o.cpu().numpy()
+            cells[part] = cl.cpu().numpy()
+            times[g] = (t0, time.monotonic())
+
         def runner(gs, idx):
-            parts = np.array_split(idx, len(gs))
-            for g, part in zip(gs, parts):               # one2all: the holder spreads over its devices
-                if part.size == 0:
-                    continue
-                dev = devs[g]
-                sub = dpairs[g][torch.from_numpy(part).to(dev)]
-                o = torch.zeros((part.size, 5), dtype=torch.int32, device=dev)
-                cl = torch.zeros(part.size, dtype=torch.int64, device=dev)
-                als[g].align_device(res_seq[g], res_off[g], sub, o, cl, **params)
-                out[part] = o.cpu().numpy()
-                cells[part] = cl.cpu().numpy()
+            # one2all: the holder splits its sub-batch over its devices and drives them CONCURRENTLY
+            # (one host thread per device), each turn timed on its own device
+            parts = [(g, p) for g, p in zip(gs, np.array_split(idx, len(gs))) if p.size]
+            times = {}
+            if len(parts) == 1:
+                run_part(parts[0][0], parts[0][1], times)
+                return times
+            errs = []
+
+            def body(g, p):
+                try:
+                    torch.cuda.set_device(devs[g])
+                    run_part(g, p, times)
+                except BaseException as e:      # noqa: BLE001 (re-raised below)
+                    errs.append(e)
+            ths = [threading.Thread(target=body, args=gp) for gp in parts]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            if errs:
+                raise errs[0]
+            return times
     else:
         def runner(gs, idx):
             time.sleep(sleep_ns_per_pair * idx.size * 1e-9)

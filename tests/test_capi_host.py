@@ -116,3 +116,45 @@ def test_one2one_concurrency_and_cells_balance(xd):
     _, _, gpu = xd.sched_simulate(4, "cells", 1, w)
     loads = np.bincount(gpu, weights=w, minlength=4)
     assert loads.max() - loads.min() <= w.max()                   # LPT bound
+
+
+def _sass_opcode_counts(cubin):
+    """{function: {opcode: count}} of a cubin (cuobjdump -sass)."""
+    import subprocess
+    txt = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True, check=True).stdout
+    out, fn = {}, None
+    for line in txt.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            fn = m.group(1)
+            out[fn] = {}
+            continue
+        m = re.match(r"\s*/\*[0-9a-f]+\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Za-z0-9_.]*)", line)
+        if m and fn:
+            out[fn][m.group(1)] = out[fn].get(m.group(1), 0) + 1
+    return out
+
+
+def test_peak_probes_sass(tmp_path):
+    """The roofline denominators (csrc/xdrop_peaks.cu): each probe's loop is the ONE named SASS
+    instruction (>= 95% of the kernel's instructions; 80% for the two-pipe mix, whose loop ptxas does not unroll further), so its measured rate is that pipe's rate."""
+    import subprocess
+    cubin = str(tmp_path / "peaks.cubin")
+    subprocess.run(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-o",
+                    cubin, os.path.join(ROOT, "paper_2309_07270_b200", "csrc", "xdrop_peaks.cu")], check=True)
+    counts = _sass_opcode_counts(cubin)
+    want = {"0": {"VIMNMX3.S16x2"}, "1": {"VIMNMX3"}, "2": {"LOP3.LUT"}, "3": {"IADD3"}, "4": {"IMAD"},
+            "5": {"VIMNMX3.S16x2", "IMAD"}}
+    seen = set()
+    for fn, c in counts.items():
+        m = re.search(r"peak_kernelILi(\d)E", fn)
+        if not m:
+            continue
+        seen.add(m.group(1))
+        total = sum(c.values())
+        named = sum(v for k, v in c.items() if k in want[m.group(1)])
+        # (the mix loop is not unrolled further by ptxas: ~55 prologue/epilogue instructions around the 257-instruction loop)
+        assert named >= (0.8 if m.group(1) == "5" else 0.95) * total, (m.group(1), c)
+        if m.group(1) == "5":
+            assert abs(c["IMAD"] - c["VIMNMX3.S16x2"]) <= 0.05 * named, c
+    assert seen == set(want), seen

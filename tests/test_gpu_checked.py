@@ -13,6 +13,26 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB_CHECKED = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
+
+
+def child_env(lib, **extra):
+    """The child's environment: the library under test plus the repo on PYTHONPATH, APPENDED to the
+    inherited one (the driver's load hooks travel in the parent's environment)."""
+    pp = os.environ.get("PYTHONPATH", "")
+    return {**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT + (os.pathsep + pp if pp else ""), **extra}
+
+
+@pytest.fixture(scope="module")
+def checked_lib():
+    """libxdrop_checked.so, built here if missing (every test of this module uses it)."""
+    sys.path.insert(0, os.path.join(ROOT, "paper_2309_07270_b200"))
+    try:
+        import build as B
+        B.build_checked(verbose=True)
+    finally:
+        sys.path.pop(0)
+    return LIB_CHECKED
 
 CHILD = textwrap.dedent("""
     import numpy as np
@@ -46,22 +66,16 @@ CHILD = textwrap.dedent("""
 """)
 
 
-def test_checked_build_every_path():
-    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
-    if not os.path.exists(lib):
-        sys.path.insert(0, os.path.join(ROOT, "paper_2309_07270_b200"))
-        import build as B
-        B.build_checked(verbose=True)
+def test_checked_build_every_path(checked_lib):
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True, timeout=900,
-                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT})
+                       env=child_env(checked_lib))
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
     assert "checked ok 21" in r.stdout
 
 
-def test_checked_build_traps_out_of_bounds_reads():
+def test_checked_build_traps_out_of_bounds_reads(checked_lib):
     """The checker itself: with only the guard band registered, the first real read must trap and the
     call must fail with XDROP_ECUDA (-3), not return results."""
-    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
     child = textwrap.dedent("""
         import paper_2309_07270_b200 as xd
         from synth import workload as W
@@ -74,9 +88,8 @@ def test_checked_build_traps_out_of_bounds_reads():
             print("status", e.status)
     """)
     r = subprocess.run([sys.executable, "-c", child], cwd=ROOT, capture_output=True, text=True, timeout=300,
-                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT, "XDROP_CHK_SHRINK": "1"})
-    assert "status -3" in r.stdout or ("status" in r.stdout and "no trap" not in r.stdout), \
-        (r.stdout[-2000:], r.stderr[-2000:])
+                       env=child_env(checked_lib, XDROP_CHK_SHRINK="1"))
+    assert "status -3" in r.stdout.split("\n"), (r.stdout[-2000:], r.stderr[-2000:])
 
 
 CHILD_FULL = textwrap.dedent("""
@@ -89,7 +102,9 @@ CHILD_FULL = textwrap.dedent("""
         w = W.config(name, scale=scale, X=X)
         with xd.Aligner() as al:
             res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
-        idx = np.linspace(0, w.n_pairs - 1, min(w.n_pairs, 600)).astype(np.int64)
+        # E. coli (the benched batch): every pair; the others: 600 evenly spaced pairs
+        n_chk = w.n_pairs if name == "ecoli" else min(w.n_pairs, 600)
+        idx = np.linspace(0, w.n_pairs - 1, n_chk).astype(np.int64)
         ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs[idx], w.k, w.M, w.mu, w.g, w.X)
         for f in F:
             assert np.array_equal(res[f][idx], ref[f]), (name, f)
@@ -99,11 +114,10 @@ CHILD_FULL = textwrap.dedent("""
 """)
 
 
-def test_checked_build_config_workloads():
-    """The bench's full E. coli-shaped batch (the launch configuration bench.py times) and small
-    C. elegans-shaped / X = 100 sweep batches through the bounds-checked build: no trap, sampled pairs
-    bit-exact against the oracle."""
-    lib = os.path.join(ROOT, "paper_2309_07270_b200", "libxdrop_checked.so")
+def test_checked_build_config_workloads(checked_lib):
+    """The bench's full E. coli-shaped batch (the launch configuration bench.py times; every pair
+    bit-exact) and small C. elegans-shaped / X = 100 sweep batches (sampled pairs bit-exact) through
+    the bounds-checked build: no trap."""
     r = subprocess.run([sys.executable, "-c", CHILD_FULL], cwd=ROOT, capture_output=True, text=True, timeout=900,
-                       env={**os.environ, "XDROP_LIB": lib, "PYTHONPATH": ROOT})
+                       env=child_env(checked_lib))
     assert r.returncode == 0 and "full ok" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
