@@ -189,7 +189,8 @@ def ncu_traffic(args, kregex):
         if len(row) >= 3 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
             unit, val = row[-2], float(row[-1].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
-                     "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1)
+                     "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+                     "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}.get(unit, 1)
             vals[row[-3]] = val * scale
     if "dram__bytes_read.sum" not in vals:
         return None, f"ncu gave no DRAM metrics (rc {r.returncode}): {(r.stdout + r.stderr)[-300:]!r}"

@@ -90,9 +90,10 @@ typedef struct {
 #define XDROP_FLAG_FORCE_WIDE 1    /* skip the lane-per-extension path (tests) */
 #define XDROP_FLAG_FORCE_GENERAL 2 /* send every extension to the unbounded fallback (tests) */
 #define XDROP_FLAG_NO_SORT 4       /* do not length-sort the work queue (tests) */
-/* Packed-mode band kernel (X + M <= 510).  Default: chosen per call from the previous
- * call's escalation count on the device (the shared kernel once escalated work alone can fill the
- * GPU's resident warps, else the tiered one); results are identical either way. */
+/* Packed-mode band kernel (X + M <= 510).  Default: chosen per batch on the device by
+ * a probe (up to 4096 evenly spaced extensions of the batch run for <= 256 anti-diagonals in the T0
+ * window; the shared kernel when the predicted T0 -> T1 escalations reach 1024, else the tiered
+ * one); results are identical either way. */
 #define XDROP_FLAG_TIERED 8        /* always the tiered kernel (small per-tier loops, short tails) */
 #define XDROP_FLAG_SHARED 16       /* always the shared kernel (one loop for every tier, no I$ thrash) */
 
@@ -187,6 +188,7 @@ typedef struct {
   int64_t cta_items;      /* extensions checkpointed into the S = 2048 thread-block level */
   int64_t cta4k_items;    /* extensions checkpointed into the S = 4096 thread-block level */
   int64_t endgame_stolen; /* shared kernel: T1/T2 extensions moved to the 32 x 8 shape at the tail */
+  int64_t probe_overflows; /* per-batch kernel probe: sampled extensions that outgrew the T0 window */
 } xdrop_stats;
 int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st);
 

@@ -26,7 +26,7 @@ class Aligner:
 
     def __init__(self, n_devices: int = 1, devices=None, policy: str = "cells", n_ranks: int = 1,
                  batch_size: int = 10000, subbatches: int = 1, flags: int = 0, kernel: str = "auto"):
-        """kernel: packed band kernel -- "auto" (per call from the previous call's escalations),
+        """kernel: packed band kernel -- "auto" (per batch, from the on-device probe's escalation estimate),
         "tiered" or "shared" (XDROP_FLAG_TIERED / XDROP_FLAG_SHARED)."""
         flags |= N.KERNELS[kernel]
         opts = N.InitOpts()
@@ -165,7 +165,8 @@ class Aligner:
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
                     level_cells=list(s.level_cells), level_items=list(s.level_items),
                     long_items=s.long_items, stolen=s.stolen,
-                    band_kernel=("merged32", "tiered", "shared")[s.band_kernel], cta_items=s.cta_items, cta4k_items=s.cta4k_items, endgame_stolen=s.endgame_stolen)
+                    band_kernel=("merged32", "tiered", "shared")[s.band_kernel], cta_items=s.cta_items, cta4k_items=s.cta4k_items, endgame_stolen=s.endgame_stolen,
+                    probe_overflows=s.probe_overflows)
 
     def sched_stats(self) -> dict:
         s = N.SchedStats()

@@ -44,7 +44,8 @@ class Stats(ctypes.Structure):
                 ("kernel_ms", ctypes.c_float), ("total_ms", ctypes.c_float), ("pack_ms", ctypes.c_float),
                 ("launches", ctypes.c_int64), ("level_ms", ctypes.c_float * 4),
                 ("level_cells", ctypes.c_int64 * 4), ("level_items", ctypes.c_int64 * 4),
-                ("long_items", ctypes.c_int64), ("stolen", ctypes.c_int64), ("band_kernel", ctypes.c_int64), ("cta_items", ctypes.c_int64), ("cta4k_items", ctypes.c_int64), ("endgame_stolen", ctypes.c_int64)]
+                ("long_items", ctypes.c_int64), ("stolen", ctypes.c_int64), ("band_kernel", ctypes.c_int64), ("cta_items", ctypes.c_int64), ("cta4k_items", ctypes.c_int64), ("endgame_stolen", ctypes.c_int64),
+                ("probe_overflows", ctypes.c_int64)]
 
 
 class TraceEvent(ctypes.Structure):

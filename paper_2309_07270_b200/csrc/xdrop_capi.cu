@@ -71,14 +71,17 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_TLN,                                               // timeline records
        C_ZERO,                                              // always 0 (an empty queue's tail)
        C_WP, C_WT, C_WH, C_WD,                              // endgame steals of the shared kernel
+       C_PROBE, C_PROBEFB,                                  // per-batch kernel probe: overflows, list tail
        C_N };
 constexpr int kTimelineCap = 1 << 16;
-// Per-call choice of the packed kernel: the shared kernel once the previous call had
-// at least kSharedT1 T0 -> T1 checkpoints (escalated work is then a large or long-running part of
-// the batch: its T1/T2 pools and endgame steals beat the tiered kernel's per-tier loops) or at
-// least kSharedT3 S1024 checkpoints (it resumes them as tier T3 while the other tiers drain)
+// Per-batch choice of the packed kernel: the shared kernel when the batch's probe
+// (pk_probe_kernel: kProbe evenly spaced extensions run for at most 2 * kProbeCap anti-diagonals in
+// the T0 window) predicts at least kSharedT1 T0 -> T1 checkpoints for the whole batch (escalated
+// work is then a large or long-running part of it: the shared kernel's T1/T2 pools, endgame steals
+// and in-kernel S = 1024 tier beat the tiered kernel's per-tier loops), else the tiered kernel.
 constexpr int64_t kSharedT1 = 1024;
-constexpr int64_t kSharedT3 = 256;
+constexpr int kProbe = 4096;
+constexpr int kProbeCap = 128;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 64, HS_LVL = 80, HS_BYTES = 512 };
 static_assert(int(C_N) <= int(HS_BAD) && HS_LVL + 16 <= HS_BYTES / 4, "host mirror layout: counters, bad flags, level sums");
@@ -104,9 +107,9 @@ struct DevCtx {
   int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
-  int64_t last_t1 = 0;      // T0 -> T1 checkpoints of the previous packed call (kernel choice)
-  int64_t last_t3 = 0;      // T2 -> S1024 checkpoints of the previous packed call (kernel choice)
-  int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per call
+  int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per batch (probe)
+  int probe_thr = 0;         // last packed call: probe threshold (0: shared forced, 2^30: tiered forced)
+  int probe_choice = 0;      // last packed call: 0 probe decided, 1 tiered forced, 2 shared forced
   int age_us = 20;           // T1/T2 batch claims go partial once the oldest record waited this long (XDROP_AGE_US)
   int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
   int t0_per_sm = 3;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
@@ -114,7 +117,7 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw, probe;
   xk::PkTier tier_host[5];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
@@ -198,7 +201,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw, &D.probe};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -345,7 +348,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
                        ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
                        (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * t0b * 4 * 32), 1 << 30),
-                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns, D.age_us};
+                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns, D.age_us, ctr + C_PROBE, 0};
       CK(cudaMemsetAsync(D.smcnt.p, 0, 1024 * sizeof(int), s));
       if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
         CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
@@ -378,29 +381,46 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 5 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
         tiers = D.escbuf.as<xk::PkTier>();
       }
-      // packed kernel per call: the shared one when the previous call on this device
-      // checkpointed at least kSharedT1 extensions out of T0 (or kSharedT3 into S = 1024), else the
-      // tiered one (also for a context's first call)
-      int shared = 0;
-      if (pk) {
-        shared = fl.shared ? 1 : fl.tiered ? 0 : D.kernel_env ? (D.kernel_env == 2)
-                 : (D.last_t1 >= kSharedT1 || (D.shared_t3 && D.last_t3 >= kSharedT3));
+      // packed kernel per batch: forced by flag / XDROP_KERNEL, else the probe decides on
+      // the device (both kernels are launched; the one not chosen exits at once, so the host never
+      // waits for the probe)
+      int choice = 0;             // 0 probe, 1 tiered, 2 shared
+      if (pk) choice = fl.shared ? 2 : fl.tiered ? 1 : (D.kernel_env == 1 || D.kernel_env == 2) ? D.kernel_env : 0;
+      if (pk && choice == 0 && n_items < kSharedT1) choice = 1;   // too few extensions to reach the threshold
+      if (pk && choice == 0) {
+        const int stride = (int)std::max<int64_t>(1, n_items / kProbe);
+        const int n_probe = (int)std::min<int64_t>(kProbe, (n_items + stride - 1) / stride);
+        CKR(D.probe.ensure((size_t)kProbe * sizeof(int)));
+        xk::Esc ep{nullptr, 0, 0, ctr + C_PROBE, nullptr, nullptr, D.probe.as<int>(), ctr + C_PROBEFB};
+        xk::pk_probe_kernel<32><<<(unsigned)((n_probe + 127) / 128), 128, 0, s>>>(P, items0, ctr + C_NITEMS, n_probe,
+                                                                                  stride, kProbeCap, ep);
+        ++launches;
+        // shared iff probe overflows x (n_items / n_probe) >= kSharedT1
+        mc.probe_thr = (int)std::max<int64_t>(1, (kSharedT1 * n_probe + n_items - 1) / n_items);
+      } else {
+        mc.probe_thr = choice == 2 ? 0 : (1 << 30);
       }
-      D.st.band_kernel = pk ? 1 + shared : 0;
-      if (pk && shared && D.long_g == 2)
-        xk::pk_merged_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
-      else if (pk && shared)      // long_g 4, or 1 (no long mode: n_long = 0)
-        xk::pk_merged_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
-      else if (pk && D.long_g == 2)
+      const bool run_tiered = pk && choice != 2, run_shared = pk && choice != 1;
+      D.st.band_kernel = pk ? (choice == 2 ? 2 : 1) : 0;   // refined from the probe count after the call
+      if (run_tiered && D.long_g == 2)
         xk::pk_tiered_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (pk)
+      else if (run_tiered)
         xk::pk_tiered_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (D.long_g == 2)
+      if (run_shared && D.long_g == 2)
+        xk::pk_merged_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+      else if (run_shared)      // long_g 4, or 1 (no long mode: n_long = 0)
+        xk::pk_merged_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+      if (run_tiered && run_shared) ++launches;
+      if (pk) {
+        D.probe_thr = mc.probe_thr;
+        D.probe_choice = choice;
+      } else if (D.long_g == 2) {     // 32-bit cells (X + M > 510)
         xk::band_merged_kernel<32, 2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (D.long_g == 4)
+      } else if (D.long_g == 4) {
         xk::band_merged_kernel<32, 4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else
+      } else {
         xk::band_merged_kernel<32, 1, 32><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      }
       ++launches;
     }
     CK(cudaEventRecord(D.ev[8], s));
@@ -439,7 +459,10 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
     D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_P1];
     D.st.escalated[1] = hs[C_P2];
-    if (pk && !fl.force_wide && !fl.force_general) { D.last_t1 = hs[C_P1]; D.last_t3 = hs[C_P3]; }
+    if (pk && !fl.force_wide && !fl.force_general && D.probe_choice == 0) {
+      D.st.band_kernel = hs[C_PROBE] >= D.probe_thr ? 2 : 1;   // which kernel the probe let run
+      D.st.probe_overflows = hs[C_PROBE];
+    }
     D.st.escalated[2] = hs[C_P3];
     D.st.cta_items = hs[C_P4];
     D.st.cta4k_items = hs[C_P5];
@@ -655,6 +678,7 @@ void stats_add(xdrop_stats& a, const xdrop_stats& b) {
   a.pack_ms = std::max(a.pack_ms, b.pack_ms);
   a.long_items += b.long_items; a.stolen += b.stolen; a.band_kernel = b.band_kernel;
   a.cta_items += b.cta_items; a.cta4k_items += b.cta4k_items; a.endgame_stolen += b.endgame_stolen;
+  a.probe_overflows += b.probe_overflows;
 }
 
 struct DevSession {

@@ -763,7 +763,9 @@ struct MergedCtr { int* head0; int* done0; int* head_long; int* n_long; int* q1_
                    unsigned long long* tl; int* tl_n; int tl_cap;     // optional work-unit timeline
                    int endgame;                                       // T0 items left -> 4-lane dispatch
                    int* smcnt; int t0_per_sm; int idle_ns;
-                   int age_us; };                     // batch claims of T1/T2 go partial after this wait                      // blocks per SM that take T0 work
+                   int age_us;                        // batch claims of T1/T2 go partial after this wait
+                   const int* probe_cnt; int probe_thr; };  // packed kernels: the shared one runs iff
+                                                             // *probe_cnt >= probe_thr, the tiered one iff not
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -976,6 +978,7 @@ __global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
 pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  const PkTier* tiers, Steal st) {
   static_assert(GL * CL == 32, "4-lane units keep the lane window");
+  if (*c.probe_cnt < c.probe_thr) return;            // the batch's probe chose the tiered kernel
   enum { NONE = 0, FRESH, T1, T2, T3, STOLEN, LONG, WIDE };
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
@@ -1086,6 +1089,7 @@ template <int GL, int CL>
 __global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
 pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  Esc e1, Esc e2, Esc e3, Steal st) {
+  if (*c.probe_cnt >= c.probe_thr) return;           // the batch's probe chose the shared kernel
   const int lane = threadIdx.x & 31;
   const int n_items = *n_items_ptr;
   const int n_long = min(*c.n_long, n_items);
@@ -1197,6 +1201,29 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
     __nanosleep(t0ok ? 1000 : nap);
     if (!t0ok) nap = min(2 * nap, c.idle_ns);
   }
+}
+
+// Per-batch choice of the packed band kernel: a probe runs an evenly spaced sample of
+// n_probe extensions of the length-sorted queue in the T0 lane mode (one lane each, the T0 window)
+// for at most 2 * cap_half anti-diagonals (m, n capped; results it writes are overwritten by the
+// band kernel that follows) and counts the extensions whose band outgrows the window (cnt: an Esc
+// with no record pool, so pk_save only counts).  The two packed kernels launched after it read the
+// count and all but one exit at once: escalated work is then predicted from the batch itself, not
+// from the previous call.
+template <int C>
+__global__ void __launch_bounds__(128)
+pk_probe_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, int n_probe,
+                int stride, int cap_half, Esc cnt) {
+  const int n_items = *n_items_ptr;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  int item = -1;
+  if (gid < n_probe && (int64_t)gid * stride < n_items) item = items[(int64_t)gid * stride];
+  Band16<C> B;
+  pk_keys<C>(B, 1, 0, P.keym >> 8);
+  pk_init_seed<C>(B, 1, 0, item, P);
+  B.m = min(B.m, cap_half);
+  B.n = min(B.n, cap_half);
+  pk_loop<C>(B, 1, 0, 0, P, 0, cnt, nullptr);
 }
 
 // ------------------------------------------------------------ CTA path

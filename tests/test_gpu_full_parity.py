@@ -62,6 +62,7 @@ def test_ecoli_every_pair(xd, ecoli):
     res, cells, kernels = run_device(xd, w)
     assert_same(res, cells, ref, rcells, f"ecoli all pairs ({kernels})")
     assert int(cells.sum()) == int(rcells.sum())
+    assert kernels == ["tiered", "tiered"]      # the probe predicts few escalations (no spurious pairs)
 
 
 @pytest.fixture(scope="module")
@@ -77,6 +78,7 @@ def test_xsweep_every_pair(xd, xsweep, X):
     res, cells, kernels = run_device(xd, w)
     ref, rcells = oracle_of(w, X=X)
     assert_same(res, cells, ref, rcells, f"xsweep X={X} all pairs ({kernels})")
+    assert kernels == ["shared", "shared"]      # 20% spurious pairs (and every band at X >= 50) escalate
 
 
 def test_ecoli_every_pair_host_api(xd, ecoli):

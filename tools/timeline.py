@@ -7,6 +7,8 @@ import paper_2309_07270_b200 as xd
 from synth import workload as W
 _nm, _, _x = (sys.argv[1] if len(sys.argv) > 1 else "ecoli").partition(":")
 w = W.config(_nm, scale=0.05) if _nm == "celegans" else W.config(_nm)
+if os.environ.get("TL_KERNEL"):
+    os.environ["XDROP_KERNEL"] = os.environ["TL_KERNEL"]
 if _x:
     w = w.with_X(int(_x))
 with xd.Aligner() as al:
