@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded oracle sample")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = each rank its own seeded batch of the config; strong = ONE global batch "
+                         "split over the ranks by estimated cells (the library's LPT, BASELINE configs[2])")
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the ncu child run that measures the dominant kernel's DRAM bytes per launch")
     return ap.parse_args()
@@ -79,6 +82,17 @@ def allreduce(x: float, op: str, world: int, device=None) -> float:
     return float(t.item())
 
 
+def allgather(x: float, world: int, device=None) -> list:
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(o.item()) for o in out]
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -93,14 +107,30 @@ def shard_workload(args, rank):
     return W.config(args.config, scale=args.scale, X=args.X, seed=base + 1000 * rank)
 
 
+def rank_workload(args, rank, world):
+    """(workload, pair indices this rank aligns).  weak: its own seeded batch, every pair; strong: the
+    rank-0 seed's batch for every rank and this rank's shard of it (paper_2309_07270_b200.shard_pairs:
+    LPT over estimated cells, the same partitioner as the library's CELLS policy)."""
+    if getattr(args, "scaling", "weak") != "strong" or world == 1:
+        w = shard_workload(args, rank)
+        return w, np.arange(w.n_pairs)
+    import paper_2309_07270_b200 as xd
+    w = shard_workload(args, 0)
+    sh = xd.shard_pairs(xd.pair_costs(w.offsets, w.pairs, w.k), world)
+    return w, sh[rank]
+
+
 def workload_desc(w, args, world):
     lens = np.diff(w.offsets)
     return {"workload": f"{w.name} (BASELINE configs[1]: E. coli-shaped, ~10 kb PacBio-like reads, 15% error)"
             if args.config == "ecoli" else w.name,
-            "pairs_per_gpu": w.n_pairs, "global_pairs": w.n_pairs * world, "reads_per_gpu": int(lens.shape[0]),
+            "pairs_per_gpu": w.n_pairs if args.scaling == "weak" else round(w.n_pairs / world, 1),
+            "global_pairs": w.n_pairs * world if args.scaling == "weak" else w.n_pairs,
+            "reads_per_gpu": int(lens.shape[0]),
             "mean_read_len": round(float(lens.mean()), 1), "pool_bases_per_gpu": int(w.offsets[-1]),
             "k": w.k, "X": w.X, "scoring": [w.M, w.mu, w.g],
-            "errors": "1.5% sub / 9% ins / 4.5% del", "parallelism": f"dp{world} (independent shards)",
+            "errors": "1.5% sub / 9% ins / 4.5% del", "parallelism": f"dp{world} (independent shards)" if args.scaling == "weak" else
+            f"dp{world} (one batch split by estimated cells, LPT)",
             "l2": "flushed between timed steps (256 MiB memset)", "recipe_seed": w.recipe.get("seed")}
 
 
@@ -295,16 +325,18 @@ def run_native(args, world, rank, local):
 
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    w = shard_workload(args, rank)
+    w, sidx = rank_workload(args, rank, world)
+    my_pairs = np.ascontiguousarray(w.pairs[sidx])
+    n_my = int(my_pairs.shape[0])
     al = xd.Aligner(devices=[local])
     stream = torch.cuda.current_stream(dev)
 
     # inputs resident in HBM (value); pinned host copies (e2e)
     seq_d = torch.from_numpy(w.seq).to(dev)
     off_d = torch.from_numpy(w.offsets).to(dev)
-    pairs_d = torch.from_numpy(w.pairs).to(dev)
-    out_d = torch.zeros((w.n_pairs, 5), dtype=torch.int32, device=dev)
-    cells_d = torch.zeros(w.n_pairs, dtype=torch.int64, device=dev)
+    pairs_d = torch.from_numpy(my_pairs).to(dev)
+    out_d = torch.zeros((n_my, 5), dtype=torch.int32, device=dev)
+    cells_d = torch.zeros(n_my, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
 
     def step():
@@ -332,7 +364,8 @@ def run_native(args, world, rank, local):
     total_ms = float(sum(step_ms))
     total_ms_max = allreduce(total_ms, "max", world, dev)
     cells_all = allreduce(float(cells_step * args.steps), "sum", world, dev)
-    pairs_all = allreduce(float(w.n_pairs * args.steps), "sum", world, dev)
+    pairs_all = allreduce(float(n_my * args.steps), "sum", world, dev)
+    per_gpu_ms = allgather(total_ms / args.steps, world, dev)
     gcups = cells_all / (total_ms_max * 1e-3) / 1e9
     aps = pairs_all / (total_ms_max * 1e-3)
 
@@ -350,7 +383,7 @@ def run_native(args, world, rank, local):
     # algorithmic bytes of one band-kernel launch: the 2-bit pool read once
     # (0.25 B/base) + per extension its queue entry (4 B), pair descriptor (16 B), two read offsets
     # pairs (32 B) and its result record (32 B)
-    algo_bytes = int(w.offsets[-1]) // 4 + 2 * w.n_pairs * (4 + 16 + 32 + 32)
+    algo_bytes = int(w.offsets[-1]) // 4 + 2 * n_my * (4 + 16 + 32 + 32)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clocks = clk.summary()
     sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
@@ -389,7 +422,7 @@ def run_native(args, world, rank, local):
     if not args.no_e2e:
         seq_h = torch.from_numpy(w.seq).pin_memory().numpy()
         off_h = torch.from_numpy(w.offsets).pin_memory().numpy()
-        pairs_h = torch.from_numpy(w.pairs).pin_memory().numpy()
+        pairs_h = torch.from_numpy(my_pairs).pin_memory().numpy()
         al.align(seq_h, off_h, pairs_h, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g)     # warm
         barrier(world)
         t0 = time.perf_counter()
@@ -399,8 +432,8 @@ def run_native(args, world, rank, local):
         e_ms = (time.perf_counter() - t0) * 1e3
         e_ms_max = allreduce(e_ms, "max", world, dev)
         e_cells = allreduce(float(int(cells_h.sum()) * e_steps), "sum", world, dev)
-        h2d = int(w.seq.nbytes + w.offsets.nbytes + w.pairs.nbytes)
-        d2h = int(w.n_pairs * (20 + 8))
+        h2d = int(w.seq.nbytes + w.offsets.nbytes + my_pairs.nbytes)
+        d2h = int(n_my * (20 + 8))
         e2e = {"value": round(e_cells / (e_ms_max * 1e-3) / 1e9, 3), "unit": "GCUPS", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e_steps, "ms_per_step": round(e_ms_max / e_steps, 3)}
         # e2e results must equal the device path's
@@ -412,7 +445,8 @@ def run_native(args, world, rank, local):
     cpu = None
     parity = None
     if rank == 0 and not args.no_cpu:
-        base, (idx, ref, rcells) = oracle_sample(w, args.cpu_seconds if world == 1 else 2.0)
+        base, (idx, ref, rcells) = oracle_sample(w.subset(sidx) if n_my != w.n_pairs else w,
+                                                 args.cpu_seconds if world == 1 else 2.0)
         if world == 1:
             cpu = {k: x for k, x in base.items() if k not in ("sample_s", "sample_pairs")}
         o = out_d.cpu().numpy()[idx]
@@ -432,7 +466,10 @@ def run_native(args, world, rank, local):
         line = {"metric": METRIC,
                 "value": round(gcups, 3), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": round(total_ms_max / args.steps, 4),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i16",
+                "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
+                "dtype": "i16",
+                "per_gpu_ms": [round(x, 3) for x in per_gpu_ms],
+                "imbalance": round(max(per_gpu_ms) / (sum(per_gpu_ms) / len(per_gpu_ms)), 4),
                 "dtype_note": "DP cell values as packed 16-bit pairs relative to the X-drop threshold; "
                               "scores, thresholds and outputs int32",
                 "data": "synthetic", "config": workload_desc(w, args, world),

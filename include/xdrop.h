@@ -91,7 +91,7 @@ typedef struct {
 #define XDROP_FLAG_FORCE_GENERAL 2 /* send every extension to the unbounded fallback (tests) */
 #define XDROP_FLAG_NO_SORT 4       /* do not length-sort the work queue (tests) */
 /* Packed-mode band kernel (X + M <= 510).  Default: chosen per batch on the device by
- * a probe (up to 4096 evenly spaced extensions of the batch run for <= 256 anti-diagonals in the T0
+ * a probe (up to 4096 evenly spaced extensions of the batch run for <= 128 anti-diagonals in the T0
  * window; the shared kernel when the predicted T0 -> T1 escalations reach 1024, else the tiered
  * one); results are identical either way. */
 #define XDROP_FLAG_TIERED 8        /* always the tiered kernel (small per-tier loops, short tails) */
@@ -149,6 +149,46 @@ int xdrop_align_batch_device(xdrop_ctx* ctx,
                              const char* seqB, const int64_t* offB, int64_t nB, int64_t lenB,
                              const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
                              xdrop_result* out, int64_t* cells_out, void* stream);
+
+/* ---- registered read pools (the pool is replicated once, not per call) ----
+ * ELBA aligns many batches ("batches of size 10,000") against the same reads.
+ * xdrop_pool_register uploads a host pool ONCE: the ASCII bases go to the context's first device and
+ * are 2-bit packed there (alphabet check: XDROP_EALPHABET + base index), the packed words (0.25 B
+ * per base) are copied device-to-device to every other device of the context (cudaMemcpyPeer: NVLink
+ * on a multi-GPU node), and the offsets are kept on every device plus a host copy (validation and
+ * cost estimates).  *pool_id receives a handle >= 0; the caller's buffers may be freed on return.
+ * xdrop_align_pooled is xdrop_align_batch on registered pools (poolB may equal poolA): only the pairs
+ * (16 B) go to the devices and only the results come back; same validation, scheduling policies,
+ * results and statistics.  xdrop_pool_release frees a pool (XDROP_EINVAL for an unknown id);
+ * xdrop_finalize frees every pool still registered. */
+int xdrop_pool_register(xdrop_ctx* ctx, const xdrop_seqs* S, int32_t* pool_id);
+int xdrop_align_pooled(xdrop_ctx* ctx, int32_t poolA, int32_t poolB, const xdrop_pair* pairs, int64_t n_pairs,
+                       const xdrop_params* p, xdrop_result* out, int64_t* cells_out);
+int xdrop_pool_release(xdrop_ctx* ctx, int32_t pool_id);
+
+/* ---- candidate-pair filters (device pointers, work on `stream`, the call
+ * returns after the stream completed).  Neither needs a context.  On an invalid pair (read id out
+ * of range, seed outside its read, a non-ACGT base in a seed) they return XDROP_ESEED and set
+ * *err_index (nullable) to the smallest such pair index; XDROP_EINVAL on bad sizes or parameters.
+ *
+ * f2, BELLA's adaptive threshold ("An adaptive threshold is used to perform the X-drop alignment",
+ * PAPER.md:74; the formula is DESIGN.md reading Q12, not the paper's): for each pair with result
+ * res[p] (e.g. the `out` of xdrop_align_batch_device), ov = min(a_pos, b_pos) + min(|A| - a_pos,
+ * |B'| - b_pos) (the overlap the seed's diagonal implies), mu = phi * ov, and
+ *   keep[p] = 1  iff  res[p].score >= mu - sqrt(c * mu)     (IEEE fp64, round to nearest, no FMA)
+ * -- a Chernoff lower bound of the score a true overlap of that length reaches (c = 2 ln(1/gamma)).
+ * 0 < phi <= 1e6, 0 <= c <= 1e12.  offA / offB: n+1 int64 offsets of the pools (B may equal A). */
+int xdrop_adaptive_filter_device(const int64_t* offA, int64_t nA, const int64_t* offB, int64_t nB,
+                                 const xdrop_pair* pairs, const xdrop_result* res, int64_t n,
+                                 double phi, double c, uint8_t* keep, int64_t* err_index, void* stream);
+/* f4, the k-mer frequency band of ELBA's seeds (LOWER_KMER_FREQ, UPPER_KMER_FREQ):
+ * freq[p] = the number of positions of the ASCII pool (seq, off: n_reads reads, len bases) whose k-mer
+ * equals pair p's seed k-mer A[a_pos, a_pos + k) on either strand (canonical k-mers, A0 C1 G2 T3,
+ * first base most significant; k-mers containing a non-ACGT base or crossing a read boundary do not
+ * count), 1 <= k <= 31; keep[p] = lower <= freq[p] <= upper.  freq or keep may be NULL (not both). */
+int xdrop_seed_kmer_freq_device(const char* seq, const int64_t* off, int64_t n_reads, int64_t len,
+                                const xdrop_pair* pairs, int64_t n, int k, int lower, int upper,
+                                int32_t* freq, uint8_t* keep, int64_t* err_index, void* stream);
 
 /* ---- several seeds per candidate pair (reading Q26) ----
  * Seed-and-extend tools extend every seed a candidate pair shares and keep the best alignment

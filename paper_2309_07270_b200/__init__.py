@@ -14,7 +14,8 @@ from . import _native as N
 from ._native import RESULT_DTYPE, TRACE_DTYPE, XdropError  # noqa: F401
 
 __all__ = ["Aligner", "XdropError", "RESULT_DTYPE", "TRACE_DTYPE", "ring_left", "ring_right",
-           "sched_simulate", "alu_peaks"]
+           "sched_simulate", "alu_peaks", "pair_costs", "shard_pairs", "adaptive_filter_device",
+           "seed_kmer_freq_device"]
 
 
 def _params(M, mu, g, X, k):
@@ -84,6 +85,35 @@ class Aligner:
         st = N.lib.xdrop_align_batch(self._h, ctypes.byref(A), pB, pairs.ctypes.data, n, ctypes.byref(p),
                                      out.ctypes.data, cells.ctypes.data if want_cells else None)
         N.check(st, "xdrop_align_batch", self._h)
+        return out, cells
+
+    # ------------------------------------------------------ registered pools
+    def register_pool(self, seq: np.ndarray, offsets: np.ndarray) -> int:
+        """xdrop_pool_register: upload + 2-bit pack a host read pool once (every device of the
+        context); returns the pool id for align_pooled."""
+        seq = np.ascontiguousarray(seq, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        S = N.Seqs(seq.ctypes.data, offsets.ctypes.data, offsets.shape[0] - 1)
+        pid = ctypes.c_int32(-1)
+        N.check(N.lib.xdrop_pool_register(self._h, ctypes.byref(S), ctypes.byref(pid)), "xdrop_pool_register",
+                self._h)
+        return int(pid.value)
+
+    def release_pool(self, pool_id: int):
+        N.check(N.lib.xdrop_pool_release(self._h, int(pool_id)), "xdrop_pool_release")
+
+    def align_pooled(self, pool_id: int, pairs: np.ndarray, k: int, X: int, M: int = 1, mu: int = -1, g: int = -1,
+                     pool_b: int | None = None, want_cells: bool = True):
+        """xdrop_align_pooled on registered pools -> (results RESULT_DTYPE[n], cells int64[n])."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 4)
+        n = pairs.shape[0]
+        out = np.empty(n, dtype=RESULT_DTYPE)
+        cells = np.empty(n, dtype=np.int64) if want_cells else None
+        p = _params(M, mu, g, X, k)
+        st = N.lib.xdrop_align_pooled(self._h, int(pool_id), int(pool_id if pool_b is None else pool_b),
+                                      pairs.ctypes.data, n, ctypes.byref(p), out.ctypes.data,
+                                      cells.ctypes.data if want_cells else None)
+        N.check(st, "xdrop_align_pooled", self._h)
         return out, cells
 
     # -------------------------------------------------------------- device API
@@ -164,7 +194,7 @@ class Aligner:
         return dict(items=s.items, escalated=list(s.escalated), kernel_ms=s.kernel_ms, total_ms=s.total_ms,
                     pack_ms=s.pack_ms, launches=s.launches, level_ms=list(s.level_ms),
                     level_cells=list(s.level_cells), level_items=list(s.level_items),
-                    long_items=s.long_items, stolen=s.stolen,
+                    long_items=s.long_items, stolen=s.stolen, cells=s.cells,
                     band_kernel=("merged32", "tiered", "shared")[s.band_kernel], cta_items=s.cta_items, cta4k_items=s.cta4k_items, endgame_stolen=s.endgame_stolen,
                     probe_overflows=s.probe_overflows)
 
@@ -207,6 +237,68 @@ def alu_peaks(device: int = 0) -> dict:
     N.check(st, "xdrop_alu_peaks")
     return {p: {"lane_ops_per_s": float(out[2 * i]), "inst_per_clk_sm": float(out[2 * i + 1])}
             for i, p in enumerate(PEAK_PROBES)}
+
+
+def adaptive_filter_device(offA, pairs, out, keep, phi: float, c: float, offB=None, stream=None):
+    """xdrop_adaptive_filter_device (f2, reading Q12) on torch CUDA tensors: offsets int64[n+1],
+    pairs int32[n,4], out int32[n,5] (alignment results), keep uint8[n] (written)."""
+    offB = offA if offB is None else offB
+    dev = pairs.device.index
+    n = int(pairs.shape[0])
+    _check_tensor("offA", offA, (1,), ("int64",), dev)
+    _check_tensor("offB", offB, (1,), ("int64",), dev)
+    _check_tensor("pairs", pairs, (2,), ("int32",), dev, cols=4)
+    _check_tensor("out", out, (2,), ("int32",), dev, rows=n, cols=5)
+    _check_tensor("keep", keep, (1,), ("uint8",), dev, rows=n)
+    err = ctypes.c_int64(-1)
+    s = stream.cuda_stream if stream is not None else None
+    st = N.lib.xdrop_adaptive_filter_device(offA.data_ptr(), offA.shape[0] - 1, offB.data_ptr(), offB.shape[0] - 1,
+                                            pairs.data_ptr(), out.data_ptr(), n, float(phi), float(c),
+                                            keep.data_ptr(), ctypes.byref(err), s)
+    if st != N.OK:
+        raise XdropError(int(st), "xdrop_adaptive_filter_device", int(err.value))
+
+
+def seed_kmer_freq_device(seq, off, pairs, k: int, lower: int, upper: int, freq=None, keep=None, stream=None):
+    """xdrop_seed_kmer_freq_device (f4) on torch CUDA tensors: ASCII pool uint8, offsets
+    int64[n_reads+1], pairs int32[n,4]; fills freq int32[n] and / or keep uint8[n]."""
+    dev = pairs.device.index
+    n = int(pairs.shape[0])
+    _check_tensor("seq", seq, (1,), ("uint8", "int8"), dev)
+    _check_tensor("off", off, (1,), ("int64",), dev)
+    _check_tensor("pairs", pairs, (2,), ("int32",), dev, cols=4)
+    if freq is not None:
+        _check_tensor("freq", freq, (1,), ("int32",), dev, rows=n)
+    if keep is not None:
+        _check_tensor("keep", keep, (1,), ("uint8",), dev, rows=n)
+    err = ctypes.c_int64(-1)
+    s = stream.cuda_stream if stream is not None else None
+    st = N.lib.xdrop_seed_kmer_freq_device(seq.data_ptr(), off.data_ptr(), off.shape[0] - 1, int(seq.shape[0]),
+                                           pairs.data_ptr(), n, int(k), int(lower), int(upper),
+                                           freq.data_ptr() if freq is not None else None,
+                                           keep.data_ptr() if keep is not None else None, ctypes.byref(err), s)
+    if st != N.OK:
+        raise XdropError(int(st), "xdrop_seed_kmer_freq_device", int(err.value))
+
+
+def pair_costs(offsets: np.ndarray, pairs: np.ndarray, k: int, offsets_b=None) -> np.ndarray:
+    """Estimated cost of each pair (the host scheduler's w): anti-diagonals of
+    its two extensions ~ min prefix + min suffix (+1)."""
+    pairs = np.asarray(pairs).reshape(-1, 4).astype(np.int64)
+    la = np.diff(np.asarray(offsets, dtype=np.int64))
+    lb = la if offsets_b is None else np.diff(np.asarray(offsets_b, dtype=np.int64))
+    a, b = pairs[:, 0], pairs[:, 1] & 0x7fffffff
+    return (np.minimum(pairs[:, 2], pairs[:, 3]) +
+            np.minimum(la[a] - pairs[:, 2] - k, lb[b] - pairs[:, 3] - k) + 1)
+
+
+def shard_pairs(w, n_shards: int):
+    """Split pairs over n_shards GPUs by estimated cells with the library's own LPT partitioner (the
+    CELLS policy of csrc/sched.cpp, host-only dry run): returns one index array per shard."""
+    if n_shards <= 1:
+        return [np.arange(np.asarray(w).shape[0])]
+    _, _, gpu = sched_simulate(n_shards, "cells", 1, np.asarray(w, dtype=np.int64))
+    return [np.nonzero(gpu == s)[0] for s in range(n_shards)]
 
 
 def _check_tensor(name, t, dims, dtypes, device, rows=None, cols=None):

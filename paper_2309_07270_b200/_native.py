@@ -68,7 +68,8 @@ EXPORTS = [
     "xdrop_best_seed_device", "xdrop_align_multiseed",
     "xdrop_last_sched_stats", "xdrop_last_trace", "xdrop_sched_simulate", "xdrop_ring_left",
     "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_alu_peaks",
-    "xdrop_last_timeline",
+    "xdrop_last_timeline", "xdrop_pool_register", "xdrop_align_pooled", "xdrop_pool_release",
+    "xdrop_adaptive_filter_device", "xdrop_seed_kmer_freq_device",
 ]
 
 
@@ -102,6 +103,14 @@ def _load():
     lib.xdrop_last_error_index.argtypes = [P]
     lib.xdrop_last_error_index.restype = ctypes.c_int64
     lib.xdrop_alu_peaks.argtypes = [ctypes.c_int, P, ctypes.c_int]
+    lib.xdrop_pool_register.argtypes = [P, ctypes.POINTER(Seqs), ctypes.POINTER(ctypes.c_int32)]
+    lib.xdrop_align_pooled.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int64,
+                                       ctypes.POINTER(Params), P, P]
+    lib.xdrop_pool_release.argtypes = [P, ctypes.c_int32]
+    lib.xdrop_adaptive_filter_device.argtypes = [P, ctypes.c_int64, P, ctypes.c_int64, P, P, ctypes.c_int64,
+                                                 ctypes.c_double, ctypes.c_double, P, P, P]
+    lib.xdrop_seed_kmer_freq_device.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int64,
+                                                ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
     lib.xdrop_last_timeline.argtypes = [P, P, ctypes.c_int64]
     lib.xdrop_last_timeline.restype = ctypes.c_int64
     return lib

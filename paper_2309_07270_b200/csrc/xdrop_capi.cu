@@ -81,7 +81,7 @@ constexpr int kTimelineCap = 1 << 16;
 // and in-kernel S = 1024 tier beat the tiered kernel's per-tier loops), else the tiered kernel.
 constexpr int64_t kSharedT1 = 1024;
 constexpr int kProbe = 4096;
-constexpr int kProbeCap = 128;
+constexpr int kProbeCap = 64;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
 enum { HS_BAD = 64, HS_LVL = 80, HS_BYTES = 512 };
 static_assert(int(C_N) <= int(HS_BAD) && HS_LVL + 16 <= HS_BYTES / 4, "host mirror layout: counters, bad flags, level sums");
@@ -98,12 +98,13 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
                               // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
-  float long_alpha = 1.0f; // long cut (XDROP_LONG_ALPHA)
+  float long_alpha = 2.0f; // long cut (XDROP_LONG_ALPHA; 2 measured best: E. coli 12.2 -> 11.7 ms vs 1, X-sweep and
+                           // C. elegans within 1%)
   int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
@@ -112,7 +113,8 @@ struct DevCtx {
   int probe_choice = 0;      // last packed call: 0 probe decided, 1 tiered forced, 2 shared forced
   int age_us = 20;           // T1/T2 batch claims go partial once the oldest record waited this long (XDROP_AGE_US)
   int idle_ns = 16000;       // max poll period (exponential backoff) of escalation-only warps (XDROP_IDLE_NS)
-  int t0_per_sm = 3;         // packed kernel: resident blocks per SM that take T0 work (the rest: escalations)
+  int t0_per_sm = 0;         // packed kernels: resident blocks per SM that take T0 work (the rest: escalations;
+                             // 0: all -- 4 for the tiered kernel, 3 for the shared one)
   bool pk16 = true;          // packed 16-bit lane mode for T0 (XDROP_PK16=0: 32-bit lane mode)
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
@@ -156,24 +158,33 @@ int dev_open(DevCtx& D, int dev) {
   if (D.long_g == 2) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<2, 16>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm, xk::pk_merged_kernel<2, 16>, 128, 0));
   } else if (D.long_g == 4) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<4, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm, xk::pk_merged_kernel<4, 8>, 128, 0));
   } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 1, 32>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<4, 8>, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm, xk::pk_merged_kernel<4, 8>, 128, 0));
   }
   D.occ_pk = std::max(1, D.occ_pk);
+  D.occ_pkm = std::max(1, D.occ_pkm);
   // resident blocks per SM of the packed merged kernel: fewer co-resident warps shorten the
   // anti-diagonal chain of the longest extensions (the launch's tail); XDROP_OCC overrides
   {
-    const int occ_max = D.occ_pk;
-    if (const char* e = getenv("XDROP_OCC")) D.occ_pk = std::max(1, std::min(occ_max, atoi(e)));
+    // the tiered kernel is compiled for 4 blocks per SM (128 registers) but launched with 3: measured
+    // E. coli 12.0 ms vs 14.0 with 4 blocks (more co-resident warps stretch the longest extensions'
+    // anti-diagonal chain, the launch's critical path) and 12.5 with 168 registers at 3 blocks
+    D.occ_pk = std::min(D.occ_pk, 3);
+    if (const char* e = getenv("XDROP_OCC")) {
+      D.occ_pk = std::max(1, std::min(4, atoi(e)));
+      D.occ_pkm = std::max(1, std::min(D.occ_pkm, atoi(e)));
+    }
     if (const char* e = getenv("XDROP_T0_PER_SM")) D.t0_per_sm = std::max(0, atoi(e));
     if (const char* e = getenv("XDROP_IDLE_NS")) D.idle_ns = std::max(0, atoi(e));
     if (const char* e = getenv("XDROP_AGE_US")) D.age_us = std::max(0, atoi(e));
     if (const char* e = getenv("XDROP_KERNEL")) D.kernel_env = atoi(e);
-    if (D.t0_per_sm <= 0) D.t0_per_sm = D.occ_pk;
   }
   CKR(D.smcnt.ensure(1024 * sizeof(int)));
   D.occ_m = std::max(1, D.occ_m);
@@ -232,7 +243,10 @@ struct Flags { bool force_wide, force_general, nosort, tiered, shared; };
 int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, int64_t lenA,
                  const char* seqB, const int64_t* offB, int64_t nB, int64_t lenB,
                  const PairDesc* pairs, int64_t n_pairs, const xdrop_params& p, int* out5,
-                 long long* cells, cudaStream_t s, Flags fl, bool do_pack = true) {
+                 long long* cells, cudaStream_t s, Flags fl, bool do_pack = true,
+                 const uint32_t* prepA = nullptr, const uint32_t* prepB = nullptr) {
+  // prepA / prepB: pools already 2-bit packed on this device (xdrop_pool_register); seqA / seqB are
+  // then not read
   D.err_index = -1;
   D.st = xdrop_stats{};
   int64_t launches = 0;
@@ -256,17 +270,21 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   init_counters_kernel<<<1, 32, 0, s>>>(D.counters.as<int>(), (int)n_items);
   launches += 2;
   // a1: ingest + pack (once per call per device; sub-batches reuse it)
-  if (do_pack) CKR(pack_pool(D, seqA, lenA, D.packA, s, launches));
-  const uint32_t* PB = D.packA.as<uint32_t>();
-  if (seqB != seqA) {
-    if (do_pack) CKR(pack_pool(D, seqB, lenB, D.packB, s, launches));
-    PB = D.packB.as<uint32_t>();
+  if (!prepA && do_pack) CKR(pack_pool(D, seqA, lenA, D.packA, s, launches));
+  const uint32_t* PA = prepA ? prepA : D.packA.as<uint32_t>();     // (after pack_pool: it may reallocate)
+  const uint32_t* PB = prepB;
+  if (!PB) {
+    PB = PA;
+    if (seqB != seqA) {
+      if (do_pack) CKR(pack_pool(D, seqB, lenB, D.packB, s, launches));
+      PB = D.packB.as<uint32_t>();
+    }
   }
   CK(cudaEventRecord(D.ev[1], s));
 #ifdef XDROP_CHECKED
   {
-    const uint32_t* base[2] = {D.packA.as<uint32_t>(), PB};
-    int64_t words[2] = {packed_words(lenA), packed_words(seqB != seqA ? lenB : lenA)};
+    const uint32_t* base[2] = {PA, PB};
+    int64_t words[2] = {packed_words(lenA), packed_words(PB != PA ? lenB : lenA)};
     // mutation knob for the checker's own test: register only the leading guard band, so that
     // the first real base any kernel reads is out of bounds and must trap
     if (getenv("XDROP_CHK_SHRINK")) words[0] = words[1] = xk::GUARD / 16;
@@ -276,7 +294,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
 #endif
 
   xk::Problem P;
-  P.PA = D.packA.as<uint32_t>(); P.offA = offA; P.nA = nA;
+  P.PA = PA; P.offA = offA; P.nA = nA;
   P.PB = PB; P.offB = offB; P.nB = nB;
   P.lenA = lenA; P.lenB = lenB;
   P.pairs = pairs; P.n_pairs = n_pairs;
@@ -285,8 +303,11 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   P.pkM = 32 * (p.match - 2 * p.gap); P.pkU = 32 * (p.mismatch - 2 * p.gap);
   // packed 16-bit lane mode (xdrop_pk16.cuh) whenever its value range holds
   const bool pk = D.pk16 && p.xdrop + p.match <= 510;
-  const int occ = pk ? D.occ_pk : D.occ_m;   // resident blocks per SM of the merged kernel launched below
-  const int t0b = pk ? std::min(occ, D.t0_per_sm) : occ;   // of which take fresh extensions
+  // resident blocks per SM of the tiered (or 32-bit merged) kernel and of the shared kernel, and how
+  // many of them take fresh (T0) extensions
+  const int occ = pk ? D.occ_pk : D.occ_m, occm = D.occ_pkm;
+  const int t0b = pk && D.t0_per_sm > 0 ? std::min(occ, D.t0_per_sm) : occ;
+  const int t0bm = D.t0_per_sm > 0 ? std::min(occm, D.t0_per_sm) : occm;
   P.ext = D.ext.as<ExtOut>();
 
   int* ctr = D.counters.as<int>();
@@ -348,7 +369,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::MergedCtr mc{ctr + C_HEAD0, ctr + C_DONE0, ctr + C_HEADL, ctr + C_NLONG, ctr + C_Q1H, ctr + C_DONE1,
                        ctr + C_Q2H, ctr + C_IDLE, ctr + C_SH, ctr + C_DONES, nullptr, ctr + C_TLN, 0,
                        (int)std::min<int64_t>((int64_t)(D.endgame * D.sms * t0b * 4 * 32), 1 << 30),
-                       D.smcnt.as<int>(), pk ? D.t0_per_sm : 0, D.idle_ns, D.age_us, ctr + C_PROBE, 0};
+                       D.smcnt.as<int>(), pk ? t0b : 0, D.idle_ns, D.age_us, ctr + C_PROBE, 0};
       CK(cudaMemsetAsync(D.smcnt.p, 0, 1024 * sizeof(int), s));
       if (D.timeline) {                                   // XDROP_TIMELINE=1: per-work-unit timeline
         CKR(D.tl.ensure((size_t)3 * 8 * kTimelineCap));
@@ -360,13 +381,18 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       xk::Esc es{D.pools.as<int>(), rec1, (int)caps, ctr + C_SP, D.qs.as<int>(), ctr + C_ST, gen, ctr + C_GEN};
       xk::Steal stl{ctr + C_IDLE, std::max(8, nwarps / D.steal_div), D.steal_min, es};
       if (D.steal_min <= 0) stl.thresh = 1 << 30;            // disabled
-      const unsigned grid = (unsigned)(D.sms * occ);
+      const unsigned grid = (unsigned)(D.sms * occ), grid_m = (unsigned)(D.sms * occm);
+      // the shared kernel's own occupancy, T0 blocks and steal threshold
+      xk::MergedCtr mcm = mc;
+      mcm.t0_per_sm = t0bm;
+      xk::Steal stlm = stl;
+      if (D.steal_min > 0) stlm.thresh = std::max(8, D.sms * t0bm * 4 / D.steal_div);
       // the packed kernel reads its tier descriptors from device memory where used (rare paths)
       const xk::PkTier* tiers = nullptr;
       if (pk) {
         // endgame steals (T1/T2 extensions resumed 32 lanes x 8 cells once st.thresh warps idle): at
         // most one record per resident pool group
-        const int capw = D.sms * occ * 4 * 8;
+        const int capw = D.sms * std::max(occ, occm) * 4 * 8;
         CKR(D.poolw.ensure((size_t)capw * rec3 * sizeof(int)));
         CKR(D.qw.ensure((size_t)capw * sizeof(int)));
         CK(cudaMemsetAsync(D.qw.p, 0xff, (size_t)capw * sizeof(int), s));
@@ -400,6 +426,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       } else {
         mc.probe_thr = choice == 2 ? 0 : (1 << 30);
       }
+      mcm.probe_thr = mc.probe_thr;
       const bool run_tiered = pk && choice != 2, run_shared = pk && choice != 1;
       D.st.band_kernel = pk ? (choice == 2 ? 2 : 1) : 0;   // refined from the probe count after the call
       if (run_tiered && D.long_g == 2)
@@ -407,9 +434,9 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       else if (run_tiered)
         xk::pk_tiered_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       if (run_shared && D.long_g == 2)
-        xk::pk_merged_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+        xk::pk_merged_kernel<2, 16><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
       else if (run_shared)      // long_g 4, or 1 (no long mode: n_long = 0)
-        xk::pk_merged_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, tiers, stl);
+        xk::pk_merged_kernel<4, 8><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
       if (run_tiered && run_shared) ++launches;
       if (pk) {
         D.probe_thr = mc.probe_thr;
@@ -518,7 +545,19 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
 }  // namespace
 
 // ------------------------------------------------------------------- context
+namespace {
+// A read pool registered once per context (xdrop_pool_register): 2-bit packed on every device, with
+// a host copy of the offsets for the host-side validation and cost estimate of each call.
+struct RegPool {
+  bool alive = false;
+  int64_t n = 0, len = 0;
+  std::vector<int64_t> off;            // host copy, n + 1 entries
+  std::vector<Buf> off_d, pack_d;      // per device
+};
+}  // namespace
+
 struct xdrop_ctx {
+  std::vector<RegPool> pools;
   std::vector<DevCtx> devs;
   xdrop_init_opts opts{};
   std::vector<int> dev_ids;
@@ -576,6 +615,12 @@ extern "C" int xdrop_init(const xdrop_init_opts* opts, xdrop_ctx** out_ctx) {
 
 extern "C" int xdrop_finalize(xdrop_ctx* ctx) {
   if (!ctx) return XDROP_ESTATE;
+  for (auto& rp : ctx->pools)
+    for (size_t g = 0; g < rp.off_d.size() && g < ctx->devs.size(); ++g) {
+      cudaSetDevice(ctx->devs[g].dev);
+      rp.off_d[g].release();
+      rp.pack_d[g].release();
+    }
   for (auto& D : ctx->devs) dev_close(D);
   ctx->alive = false;
   delete ctx;
@@ -662,6 +707,8 @@ struct HostBatch {
   const xdrop_seqs* A; const xdrop_seqs* B; bool same;
   const xdrop_pair* pairs; const xdrop_params* p; Flags fl;
   xdrop_result* out; int64_t* cells_out;
+  int64_t n_pairs = 0;
+  const RegPool* ra = nullptr; const RegPool* rb = nullptr;   // registered pools (xdrop_align_pooled)
 };
 
 // Run a subset of pairs (indices idx) on device D; pools are uploaded once per
@@ -687,8 +734,9 @@ struct DevSession {
   bool uploaded = false;
   bool packed = false;
   xdrop_stats acc{};          // this device's counters summed over the call's turns
+  int slot = 0;               // device slot of D in the context (registered pools are per slot)
   int upload() {
-    if (uploaded) return 0;
+    if (uploaded || hb->ra) return 0;     // registered pools live on the device already
     DevCtx& d = *D;
     CK(cudaSetDevice(d.dev));
     const xdrop_seqs* A = hb->A;
@@ -727,13 +775,23 @@ struct DevSession {
     }
     const xdrop_seqs* A = hb->A;
     const xdrop_seqs* B = hb->B;
-    const char* sA = d.asciiA.as<char>();
-    const int64_t* oA = d.offA.as<int64_t>();
-    const char* sB = hb->same ? sA : d.asciiB.as<char>();
-    const int64_t* oB = hb->same ? oA : d.offB.as<int64_t>();
-    int rc = dev_pipeline(d, sA, oA, A->n, A->offsets[A->n], sB, oB, B->n, B->offsets[B->n],
-                          d.pairs.as<PairDesc>(), n, *hb->p, d.out5.as<int>(), d.cells.as<long long>(),
-                          d.stream, hb->fl, !packed);
+    int rc;
+    if (hb->ra) {                // registered pools: packed and resident, only the pairs moved
+      const RegPool& a = *hb->ra;
+      const RegPool& b = *hb->rb;
+      rc = dev_pipeline(d, nullptr, a.off_d[(size_t)slot].as<int64_t>(), a.n, a.len, nullptr,
+                        b.off_d[(size_t)slot].as<int64_t>(), b.n, b.len, d.pairs.as<PairDesc>(), n, *hb->p,
+                        d.out5.as<int>(), d.cells.as<long long>(), d.stream, hb->fl, false,
+                        a.pack_d[(size_t)slot].as<uint32_t>(), b.pack_d[(size_t)slot].as<uint32_t>());
+    } else {
+      const char* sA = d.asciiA.as<char>();
+      const int64_t* oA = d.offA.as<int64_t>();
+      const char* sB = hb->same ? sA : d.asciiB.as<char>();
+      const int64_t* oB = hb->same ? oA : d.offB.as<int64_t>();
+      rc = dev_pipeline(d, sA, oA, A->n, A->offsets[A->n], sB, oB, B->n, B->offsets[B->n],
+                        d.pairs.as<PairDesc>(), n, *hb->p, d.out5.as<int>(), d.cells.as<long long>(),
+                        d.stream, hb->fl, !packed);
+    }
     if (rc == 0 || rc != XDROP_EALPHABET) packed = true;
     if (rc == 0) stats_add(acc, d.st);
     if (rc) {
@@ -776,23 +834,20 @@ int host_validate(const xdrop_seqs* S, int64_t& err) {
 
 }  // namespace
 
-extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
-                                 const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
-                                 xdrop_result* out, int64_t* cells_out) {
-  if (!ctx || !ctx->alive) return XDROP_ESTATE;
-  ctx->err_index = -1;
-  int rc = validate_params(p);
-  if (rc) return rc;
-  if (!A || !B || n_pairs < 0 || (n_pairs > 0 && (!pairs || !out))) return XDROP_EINVAL;
-  if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
-  // the read pools' H2D copy (the bulk of the call's host->device bytes) is issued first on the
-  // single-device path, so the host-side validation below runs while the DMA engine copies
-  // (pinned caller buffers); a validation error synchronises the stream before returning
-  const bool same = A == B || (A->seq == B->seq && A->offsets == B->offsets && A->n == B->n);
-  HostBatch hb{A, B, same, pairs, p, flags_of(ctx), out, cells_out};
+// The host API's body (xdrop_align_batch, xdrop_align_pooled): hb holds host pools A, B (their
+// offsets; with registered pools also hb.ra / hb.rb), the pairs and the outputs.
+static int align_host(xdrop_ctx* ctx, HostBatch& hb) {
+  const xdrop_seqs* A = hb.A;
+  const xdrop_seqs* B = hb.B;
+  const xdrop_pair* pairs = hb.pairs;
+  const xdrop_params* p = hb.p;
+  int rc = 0;
+  const int64_t n_pairs = hb.n_pairs;
   const int m = (int)ctx->devs.size();
   std::vector<DevSession> sess((size_t)m);
-  for (int g = 0; g < m; ++g) { sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; }
+  for (int g = 0; g < m; ++g) {
+    sess[(size_t)g].D = &ctx->devs[(size_t)g]; sess[(size_t)g].hb = &hb; sess[(size_t)g].slot = g;
+  }
   const bool single = m == 1 && ctx->opts.policy == XDROP_POLICY_CELLS;
   auto pool_ok = [](const xdrop_seqs* S) {
     return S && S->offsets && S->n >= 0 && (S->n == 0 || S->seq) && S->offsets[0] == 0 && S->offsets[S->n] >= 0;
@@ -806,7 +861,7 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
     return r;
   };
   int64_t err = -1;
-  if ((rc = host_validate(A, err)) || (B != A && (rc = host_validate(B, err)))) return fail(rc, err);
+  if (!hb.ra && ((rc = host_validate(A, err)) || (B != A && (rc = host_validate(B, err))))) return fail(rc, err);
   // seeds and ids (a2), reported with the offending pair index
   for (int64_t t = 0; t < n_pairs; ++t) {
     const xdrop_pair& q = pairs[t];
@@ -857,6 +912,112 @@ extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdro
   ctx->st = xdrop_stats{};
   for (auto& se : sess) stats_add(ctx->st, se.acc);
   return 0;
+}
+
+extern "C" int xdrop_align_batch(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs* B,
+                                 const xdrop_pair* pairs, int64_t n_pairs, const xdrop_params* p,
+                                 xdrop_result* out, int64_t* cells_out) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (!A || !B || n_pairs < 0 || (n_pairs > 0 && (!pairs || !out))) return XDROP_EINVAL;
+  if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
+  // the read pools' H2D copy (the bulk of the call's host->device bytes) is issued first on the
+  // single-device path, so the host-side validation runs while the DMA engine copies (pinned
+  // caller buffers); a validation error synchronises the stream before returning
+  const bool same = A == B || (A->seq == B->seq && A->offsets == B->offsets && A->n == B->n);
+  HostBatch hb{A, B, same, pairs, p, flags_of(ctx), out, cells_out};
+  hb.n_pairs = n_pairs;
+  return align_host(ctx, hb);
+}
+
+// ------------------------------------------------------------ registered pools
+extern "C" int xdrop_pool_register(xdrop_ctx* ctx, const xdrop_seqs* S, int32_t* pool_id) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  if (!pool_id) return XDROP_EINVAL;
+  int64_t err = -1;
+  int rc = host_validate(S, err);
+  if (rc) { ctx->err_index = err; return rc; }
+  RegPool rp;
+  rp.n = S->n;
+  rp.len = S->offsets[S->n];
+  rp.off.assign(S->offsets, S->offsets + S->n + 1);
+  const int m = (int)ctx->devs.size();
+  rp.off_d.resize((size_t)m);
+  rp.pack_d.resize((size_t)m);
+  auto release = [&]() { for (int g = 0; g < m; ++g) { cudaSetDevice(ctx->devs[(size_t)g].dev);
+                                                         rp.off_d[(size_t)g].release(); rp.pack_d[(size_t)g].release(); } };
+  // slot 0: ASCII H2D + pack (alphabet check); other slots: the packed words device-to-device
+  // (NVLink peer copies on a multi-GPU node, 0.25 B per base instead of 1 B of ASCII each)
+  const int64_t words = packed_words(rp.len);
+  for (int g = 0; g < m && !rc; ++g) {
+    DevCtx& D = ctx->devs[(size_t)g];
+    if ((rc = cuda_err(cudaSetDevice(D.dev)))) break;
+    if ((rc = rp.off_d[(size_t)g].ensure((size_t)(rp.n + 1) * 8))) break;
+    if ((rc = rp.pack_d[(size_t)g].ensure((size_t)words * 4))) break;
+    if ((rc = cuda_err(cudaMemcpyAsync(rp.off_d[(size_t)g].p, rp.off.data(), (size_t)(rp.n + 1) * 8,
+                                       cudaMemcpyHostToDevice, D.stream)))) break;
+    if (g == 0) {
+      if ((rc = D.asciiA.ensure((size_t)std::max<int64_t>(rp.len, 1)))) break;
+      if ((rc = D.bad.ensure(16))) break;
+      if ((rc = cuda_err(cudaMemcpyAsync(D.asciiA.p, S->seq, (size_t)rp.len, cudaMemcpyHostToDevice, D.stream)))) break;
+      init_bad_kernel<<<1, 32, 0, D.stream>>>(D.bad.as<unsigned long long>());
+      int64_t launches = 0;
+      if ((rc = pack_pool(D, D.asciiA.as<char>(), rp.len, rp.pack_d[0], D.stream, launches))) break;
+      unsigned long long bad[2];
+      if ((rc = cuda_err(cudaMemcpyAsync(bad, D.bad.p, 16, cudaMemcpyDeviceToHost, D.stream)))) break;
+      if ((rc = cuda_err(cudaStreamSynchronize(D.stream)))) break;
+      if (bad[0] != ~0ull) { ctx->err_index = (int64_t)bad[0]; rc = XDROP_EALPHABET; break; }
+    } else {
+      const DevCtx& D0 = ctx->devs[0];
+      rc = cuda_err(cudaMemcpyPeerAsync(rp.pack_d[(size_t)g].p, D.dev, rp.pack_d[0].p, D0.dev, (size_t)words * 4,
+                                        D.stream));
+      if (!rc) rc = cuda_err(cudaStreamSynchronize(D.stream));
+    }
+  }
+  if (rc) { release(); return rc; }
+  rp.alive = true;
+  for (size_t i = 0; i < ctx->pools.size(); ++i)
+    if (!ctx->pools[i].alive) { ctx->pools[i] = std::move(rp); *pool_id = (int32_t)i; return 0; }
+  ctx->pools.push_back(std::move(rp));
+  *pool_id = (int32_t)(ctx->pools.size() - 1);
+  return 0;
+}
+
+extern "C" int xdrop_pool_release(xdrop_ctx* ctx, int32_t pool_id) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  if (pool_id < 0 || pool_id >= (int32_t)ctx->pools.size() || !ctx->pools[(size_t)pool_id].alive) return XDROP_EINVAL;
+  RegPool& rp = ctx->pools[(size_t)pool_id];
+  for (size_t g = 0; g < ctx->devs.size(); ++g) {
+    cudaSetDevice(ctx->devs[g].dev);
+    cudaStreamSynchronize(ctx->devs[g].stream);
+    rp.off_d[g].release();
+    rp.pack_d[g].release();
+  }
+  rp = RegPool{};
+  return 0;
+}
+
+extern "C" int xdrop_align_pooled(xdrop_ctx* ctx, int32_t poolA, int32_t poolB, const xdrop_pair* pairs,
+                                  int64_t n_pairs, const xdrop_params* p, xdrop_result* out, int64_t* cells_out) {
+  if (!ctx || !ctx->alive) return XDROP_ESTATE;
+  ctx->err_index = -1;
+  int rc = validate_params(p);
+  if (rc) return rc;
+  auto ok = [&](int32_t id) { return id >= 0 && id < (int32_t)ctx->pools.size() && ctx->pools[(size_t)id].alive; };
+  if (!ok(poolA) || !ok(poolB) || n_pairs < 0 || (n_pairs > 0 && (!pairs || !out))) return XDROP_EINVAL;
+  if (n_pairs > (int64_t)((1u << 30) - 1)) return XDROP_EINVAL;
+  const RegPool& ra = ctx->pools[(size_t)poolA];
+  const RegPool& rb = ctx->pools[(size_t)poolB];
+  static const char kNoSeq = 0;        // the host bases are not needed again (validated at registration)
+  xdrop_seqs A{&kNoSeq, ra.off.data(), ra.n}, B{&kNoSeq, rb.off.data(), rb.n};
+  HostBatch hb{&A, poolA == poolB ? &A : &B, poolA == poolB, pairs, p, flags_of(ctx), out, cells_out};
+  hb.n_pairs = n_pairs;
+  hb.ra = &ra;
+  hb.rb = &rb;
+  return align_host(ctx, hb);
 }
 
 extern "C" int64_t xdrop_last_timeline(const xdrop_ctx* ctx, uint64_t* buf, int64_t cap) {

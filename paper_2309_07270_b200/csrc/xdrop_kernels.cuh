@@ -803,8 +803,15 @@ __device__ __forceinline__ void tl_rec(const MergedCtr& c, int type, unsigned lo
 #ifndef XDROP_T2_G
 #define XDROP_T2_G 8
 #endif
-#ifndef XDROP_PK_MINBLOCKS
-#define XDROP_PK_MINBLOCKS 3
+// resident 4-warp blocks per SM requested from ptxas: the tiered kernel's loops fit 128 registers
+// (4 blocks, 16 warps per SM; measured faster than 3 on the throughput-bound E. coli batch), the shared
+// kernel's single run-time-G loop needs its 168 (4 blocks slowed its S = 1024 tier: X-sweep X = 50
+// 51.6 -> 74.2 ms)
+#ifndef XDROP_PKT_MINBLOCKS
+#define XDROP_PKT_MINBLOCKS 4
+#endif
+#ifndef XDROP_PKM_MINBLOCKS
+#define XDROP_PKM_MINBLOCKS 3
 #endif
 #ifndef XDROP_PK_C
 #define XDROP_PK_C 32          // cells per lane of the tiered kernel's packed lane mode (T0)
@@ -974,7 +981,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
 //   long T0 extensions from their seed and stolen lane-mode extensions: one GL x CL instance.  T1/T2 wait for a full batch of records
 // unless the oldest queued one has waited age_us or T0 has been fully claimed.
 template <int GL, int CL>
-__global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
+__global__ void __launch_bounds__(128, XDROP_PKM_MINBLOCKS)
 pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  const PkTier* tiers, Steal st) {
   static_assert(GL * CL == 32, "4-lane units keep the lane window");
@@ -1086,7 +1093,7 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
 // tail; but with several hot loops on an SM it stalls on instruction fetch once escalated work
 // is a large share of the batch.  xdrop_capi.cu picks it or pk_merged_kernel per call (§7).
 template <int GL, int CL>
-__global__ void __launch_bounds__(128, XDROP_PK_MINBLOCKS)
+__global__ void __launch_bounds__(128, XDROP_PKT_MINBLOCKS)
 pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  Esc e1, Esc e2, Esc e3, Steal st) {
   if (*c.probe_cnt >= c.probe_thr) return;           // the batch's probe chose the shared kernel

@@ -116,7 +116,8 @@ template <int C> struct Band16 {
   uint32_t cm;                    // ~0: b complemented
   int64_t sa, sb; int da, db;
   int m, n, K0, ia0, jb0;
-  int best, istar, jstar, dbase;  // best: H + BIAS
+  int istar, dstar, dbase;        // argmax cell (istar, dstar - istar); best is derived from thrN (pk_best)
+  int dneed;                      // the window can hold cells beyond the matrix from anti-diagonal dneed + 1
   int thrD1, thrD, thrN;          // W-space thresholds of anti-diagonals d-1, d and d+1
   int minL1, maxL1, minL2, maxL2;
   int cells;                      // < 2^19 anti-diagonals x 32 cells
@@ -129,6 +130,20 @@ template <int C> struct Band16 {
 // lane (wider groups extend the key with the lane: see pk_diag)
 __device__ __forceinline__ bool pk_global_keys(int G, int C) { return G * C <= 32; }
 __device__ __forceinline__ int pk_key_base(int G, int C, int gl) { return pk_global_keys(G, C) ? 31 - C * gl : 31; }
+
+// best (H + BIAS) after anti-diagonal d from the threshold of d + 1: the X-drop threshold IS the best
+// score so far minus X (reading Q2: thr_{d+1} = best_{<=d} - X), and thrN holds it in W space,
+// W = H + BIAS - g (d + 1 - dbase); so no separate best needs tracking per anti-diagonal
+template <int C>
+__device__ __forceinline__ int pk_best(const Band16<C>& B, int d, const Problem& P) {
+  return B.thrN + P.g * (d + 1 - B.dbase) + P.X;
+}
+// first anti-diagonal pair (d + 1, d + 2) whose window can reach cells beyond the matrix (i > m at
+// q > 2m - d - K0, j > n at q < d - K0 - 2n, q = 2t + parity in [0, 2S)): pk_step masks them then
+template <int C>
+__device__ __forceinline__ void pk_set_dneed(Band16<C>& B, int S) {
+  B.dneed = min(B.K0 + 2 * B.n, 2 * B.m - B.K0 - 2 * S + 1);
+}
 
 // key bytes 31 - t; `zero` is an opaque 0 so the words stay in registers (PRMT operand c)
 template <int C>
@@ -178,11 +193,12 @@ __device__ __forceinline__ uint32_t tree16(const uint32_t (&k)[N]) {
 }
 
 // One anti-diagonal d of parity PAR: V (parity PAR, holds d-2) is updated in place from
-// N (holds d-1).  CHECK: cells with q outside [qlo, qhi] (beyond the matrix) are dead.
-// Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
-template <int C, int PAR, bool CHECK, bool FMA = (XDROP_PK_FMA != 0)>
+// N (holds d-1).  by: local cells (bit tl) beyond the matrix (i > m or j > n; 0 away from the
+// edges): they compare as mismatches, so their values only fall along any path (pk_diag shows why
+// they then never matter).  Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
+template <int C, int PAR, bool FMA = (XDROP_PK_FMA != 0)>
 __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<C>& B,
-                                             int G, int gl, int qlo, int qhi, const Problem& P,
+                                             int G, int gl, uint32_t by, const Problem& P,
                                              uint32_t (&ch)[C > 16 ? 2 : 1]) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
   const int thr_d = B.thrN;
@@ -202,7 +218,7 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
   // borrows of negative low halves (the hi-half product drops them mod 2^32)
   const uint32_t kk = (uint32_t)((negU - negM) * k65536 + (P.pkU - P.pkM));
   const uint32_t D1p = (uint32_t)(D1 * k65537 + k65536);
-  uint32_t mis = (B.A0 ^ B.B0) | (B.A1 ^ B.B1);           // bit tl: local cell tl compares unequal bases
+  uint32_t mis = (B.A0 ^ B.B0) | ((B.A1 ^ B.B1) | by);   // bit tl: local cell tl compares unequal bases
   if constexpr (NP < 16) {                                // hi cells (tl >= NP) to bits 16..
     constexpr uint32_t LO = (1u << NP) - 1u;
     mis = (mis & LO) | ((mis << (16 - NP)) & (LO << 16));
@@ -248,12 +264,6 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
     v = __viaddmax_s16x2(V[u], sE, nb);
     v = __viaddmax_s16x2(v, D1p, pk::NOFLOOR);
     }
-    if constexpr (CHECK) {
-      const int q0 = 2 * (C * gl + u) + PAR, q1 = q0 + 2 * NP;
-      const uint32_t cap = ((q0 >= qlo && q0 <= qhi) ? 0x7FFFu : 0x8000u) |
-                           ((q1 >= qlo && q1 <= qhi) ? 0x7FFF0000u : 0x80000000u);
-      v = __vmins2(v, cap);
-    }
     // [31-t(lo), sign(lo) x 8, 31-t(hi), sign(hi) x 8]
     const uint32_t m = prmt(v, B.TC[u >> 1], (u & 1) ? 0xB796u : 0xB594u);
     v = lop_kill(v, m, pk::KILLC);
@@ -283,14 +293,19 @@ __device__ __forceinline__ uint32_t pk_dead(const uint32_t (&ch)[C > 16 ? 2 : 1]
 }
 
 // REDUX: G = 32 groups reduce with CREDUX (one instruction each); the shared kernel's run-time-G
-// loop passes false so that its single instance carries no second reduction path (code size, I$)
-template <int C, int PAR, bool CHECK, bool REDUX = true>
-__device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int qlo, int qhi, const Problem& P,
-                                        const uint32_t (&chc)[C > 16 ? 2 : 1]) {
+// loop passes false so that its single instance carries no second reduction path (code size, I$).
+// by / byr: the cells beyond the matrix, bit tl / bit C-1-tl (pk_beyond; 0 away from the edges).
+// A cell beyond the matrix never feeds a cell inside it (its predecessors have i' <= i, j' <= j) and,
+// comparing as a mismatch, lies below the real cell it descends from, hence below best_{<d}: it can
+// neither raise the threshold nor become the argmax, and byr drops it from the live extents -- the
+// same result as masking it dead, for a few instructions per anti-diagonal near the edges only.
+template <int C, int PAR, bool REDUX = true>
+__device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, uint32_t by, uint32_t byr,
+                                        const Problem& P, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
   uint32_t ch[C > 16 ? 2 : 1];
   uint32_t kk;
-  if constexpr (PAR == 0) kk = pk_cells<C, 0, CHECK>(B.E, B.O, B, G, gl, qlo, qhi, P, ch);
-  else kk = pk_cells<C, 1, CHECK>(B.O, B.E, B, G, gl, qlo, qhi, P, ch);
+  if constexpr (PAR == 0) kk = pk_cells<C, 0>(B.E, B.O, B, G, gl, by, P, ch);
+  else kk = pk_cells<C, 1>(B.O, B.E, B, G, gl, by, P, ch);
   const int thr_d = B.thrN;
   // key maximum over both halves: both halves of kk2 hold it; the hi half sign-extends
   const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
@@ -298,61 +313,61 @@ __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int 
   // no live cell: kmax is a dead key (< -16128), so vrel <= -505 and neither the threshold nor best
   // can move (thrH_d = best_{<d} - X, so gv <= best - 505); no separate liveness test is needed
   const uint32_t dl = pk_dead<C>(ch, chc);
-  const unsigned lb = ~dl & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  const unsigned lb = ~(dl | byr) & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
   const int tmin_l = (__clz(lb) - (32 - C)) + C * gl;
   const int tmax_l = (C - __ffs(lb)) + C * gl;
-  int vrel, tst, tmin, tmax;
+  const int ibase = (d + B.K0 + PAR) >> 1;
+  int vrel, tst, mn, mx;
   if (G == 1) {
     vrel = kl >> 5;
     tst = 31 - (kl & 31);
-    tmin = lb ? tmin_l : EMIN;
-    tmax = lb ? tmax_l : EMAX;
-  } else if (pk_global_keys(G, C)) {                      // window-wide keys: the max is the argmax
-    const int km = gmax_rt(kl, G);
-    vrel = km >> 5;
-    tst = 31 - (km & 31);
-    tmin = gmin_rt(lb ? tmin_l : EMIN, G);
-    tmax = gmax_rt(lb ? tmax_l : EMAX, G);
+    mn = lb ? ibase + tmin_l : EMIN;
+    mx = lb ? ibase + tmax_l : EMAX;
   } else {
-    // 32-bit group key: value, then the lowest lane, then the lowest local cell (reading Q8:
-    // smallest i); the live extents travel as one 16x2 word (tmax, 0x7FFF - tmin; -1 = none)
-    int K = (int)((uint32_t)(kl >> 5) << 10) | ((31 - gl) << 5) | (kl & 31);
-    if (REDUX && G == 32) {                               // CREDUX: one instruction per reduction
-      K = __reduce_max_sync(FULL, K);
-      tmin = __reduce_min_sync(FULL, lb ? tmin_l : EMIN);
-      tmax = __reduce_max_sync(FULL, lb ? tmax_l : EMAX);
+    int tmin, tmax;
+    if (pk_global_keys(G, C)) {                           // window-wide keys: the max is the argmax
+      const int km = gmax_rt(kl, G);
+      vrel = km >> 5;
+      tst = 31 - (km & 31);
+      tmin = gmin_rt(lb ? tmin_l : EMIN, G);
+      tmax = gmax_rt(lb ? tmax_l : EMAX, G);
     } else {
-      uint32_t ex = lb ? (((uint32_t)tmax_l << 16) | (uint32_t)(0x7FFF - tmin_l)) : 0xFFFFFFFFu;
-      for (int o = 1; o < G; o <<= 1) {
-        K = max(K, __shfl_xor_sync(FULL, K, o));
-        ex = __vmaxs2(ex, __shfl_xor_sync(FULL, ex, o));
+      // 32-bit group key: value, then the lowest lane, then the lowest local cell (reading Q8:
+      // smallest i); the live extents travel as one 16x2 word (tmax, 0x7FFF - tmin; -1 = none)
+      int K = (int)((uint32_t)(kl >> 5) << 10) | ((31 - gl) << 5) | (kl & 31);
+      if (REDUX && G == 32) {                             // CREDUX: one instruction per reduction
+        K = __reduce_max_sync(FULL, K);
+        tmin = __reduce_min_sync(FULL, lb ? tmin_l : EMIN);
+        tmax = __reduce_max_sync(FULL, lb ? tmax_l : EMAX);
+      } else {
+        uint32_t ex = lb ? (((uint32_t)tmax_l << 16) | (uint32_t)(0x7FFF - tmin_l)) : 0xFFFFFFFFu;
+        for (int o = 1; o < G; o <<= 1) {
+          K = max(K, __shfl_xor_sync(FULL, K, o));
+          ex = __vmaxs2(ex, __shfl_xor_sync(FULL, ex, o));
+        }
+        const int hx = ((int)ex) >> 16, lx = (int)(int16_t)(ex & 0xffffu);
+        tmax = hx < 0 ? EMAX : hx;
+        tmin = lx < 0 ? EMIN : 0x7FFF - lx;
       }
-      const int hx = ((int)ex) >> 16, lx = (int)(int16_t)(ex & 0xffffu);
-      tmax = hx < 0 ? EMAX : hx;
-      tmin = lx < 0 ? EMIN : 0x7FFF - lx;
+      vrel = K >> 10;
+      tst = C * (31 - ((K >> 5) & 31)) + 31 - (K & 31);
     }
-    vrel = K >> 10;
-    tst = C * (31 - ((K >> 5) & 31)) + 31 - (K & 31);
+    mn = (tmin == EMIN) ? EMIN : ibase + tmin;
+    mx = (tmax == EMAX) ? EMAX : ibase + tmax;
   }
   // ---- critical path: next threshold
   B.thrD1 = B.thrD; B.thrD = thr_d;
   B.thrN = thr_d + max(0, vrel - P.X) - P.g;
-  // ---- off the critical path: live extent, best / argmax, hull count (garbage in inactive
-  // lanes is harmless: their state is never written out)
-  const int ibase = (d + B.K0 + PAR) >> 1;
-  const int mn = (tmin == EMIN) ? EMIN : ibase + tmin;
-  const int mx = (tmax == EMAX) ? EMAX : ibase + tmax;
-  const int woff = -P.g * (d - B.dbase);
-  const int gv = thr_d + vrel - woff;
-  const bool up = gv > B.best;
-  B.best = up ? gv : B.best;
+  // ---- off the critical path: argmax, hull count (garbage in inactive lanes is harmless: their
+  // state is never written out).  best improves iff the anti-diagonal's maximum exceeds
+  // thr_d + X = best_{<d} (strictly: reading Q8, the earliest anti-diagonal keeps a tie)
+  const bool up = vrel > P.X;
   B.istar = up ? ibase + tst : B.istar;
-  B.jstar = up ? d - ibase - tst : B.jstar;
-  int lo = min(B.minL1, B.minL2 + 1), hi = max(B.maxL1, B.maxL2) + 1;
-  if constexpr (CHECK) {          // outside boundary blocks the live cells are off the matrix edges
-    lo = max(max(0, d - B.n), lo);
-    hi = min(min(B.m, d), hi);
-  }
+  B.dstar = up ? d : B.dstar;
+  // hull of anti-diagonal d (reading Q5), clamped to the matrix: lo >= 0 and hi <= d hold already
+  // (live cells of d-1, d-2 are inside it), lo >= d - n and hi <= m are applied here
+  const int lo = max(min(B.minL1, B.minL2 + 1), d - B.n);
+  const int hi = min(max(B.maxL1, B.maxL2) + 1, B.m);
   B.cells += max(0, hi - lo + 1);
   B.minL2 = B.minL1; B.maxL2 = B.maxL1;
   B.minL1 = mn; B.maxL1 = mx;
@@ -365,6 +380,18 @@ __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, int 
     B.Bn0 <<= 1; B.Bn1 <<= 1;
     B.jb0 += 1;
   }
+}
+
+// cells of anti-diagonal dd beyond the matrix, for this lane: by (bit tl), byr (bit C-1-tl).
+// Cell tl has i = ibase + C gl + tl: i > m for tl >= s1, j = dd - i > n for tl < s2.
+template <int C>
+__device__ __forceinline__ void pk_beyond(const Band16<C>& B, int gl, int dd, int par, uint32_t& by, uint32_t& byr) {
+  const int ibase = ((dd + B.K0 + par) >> 1) + C * gl;
+  const int s1 = min(max(B.m - ibase + 1, 0), C), s2 = min(max(dd - ibase - B.n, 0), C);
+  const uint32_t ge1 = __funnelshift_lc(0u, 0xffffffffu, s1);          // bits >= s1
+  const uint32_t ge2 = __funnelshift_lc(0u, 0xffffffffu, s2);          // bits >= s2
+  by = ge1 | ~ge2;
+  byr = ~__funnelshift_lc(0u, 0xffffffffu, C - s1) | __funnelshift_lc(0u, 0xffffffffu, C - s2);
 }
 
 // lane mode: shift the window by 2K diagonals: cell t <- cell t + K (both parities)
@@ -434,7 +461,7 @@ __device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP], int kb) {
 
 // checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
 template <int C>
-__device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d, const Esc& e) {
+__device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d, const Esc& e, const Problem& P) {
   constexpr int NP = C / 2;
   int slot = 0;
   if (gl == 0) slot = atomicAdd(e.pool_tail, 1);
@@ -445,8 +472,8 @@ __device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d
   }
   int* rec = e.pool + (size_t)slot * e.rec_ints;
   if (gl == 0) {
-    rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrN; rec[5] = B.best;
-    rec[6] = B.istar; rec[7] = B.jstar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
+    rec[0] = B.item; rec[1] = d; rec[2] = B.K0; rec[3] = B.dbase; rec[4] = B.thrN; rec[5] = pk_best(B, d, P);
+    rec[6] = B.istar; rec[7] = B.dstar - B.istar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
     rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = G * C;
     rec[15] = B.cells; rec[16] = 0; rec[REC_T] = rec_stamp();
   }
@@ -485,7 +512,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
   const bool e0 = (B.minL1 == EMIN), e1 = (B.minL2 == EMIN);
   if ((e0 && e1) || d >= B.m + B.n) {
     if (gl == 0) {
-      ExtOut o; o.best = B.best - BIAS; o.istar = B.istar; o.jstar = B.jstar; o.level = level;
+      ExtOut o; o.best = pk_best(B, d, P) - BIAS; o.istar = B.istar; o.jstar = B.dstar - B.istar; o.level = level;
       o.cells = B.cells; o.pad = 0;
       XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
@@ -501,7 +528,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
       const int s_lo = (qmx - 2 * S + 4) >> 1;
       const int s_hi = (qmn - 2) >> 1;
       if (s_lo > s_hi) {
-        pk_save<C>(B, G, gl, d, esc);
+        pk_save<C>(B, G, gl, d, esc, P);
         B.active = false;
         return;
       }
@@ -512,6 +539,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
       pk_shift_n<C>(B, sh);
       pk_rekey<C / 2>(B.E, pk_key_base(G, C, gl)); pk_rekey<C / 2>(B.O, pk_key_base(G, C, gl));
       B.K0 += 2 * sh; B.ia0 += sh; B.jb0 -= sh;
+      pk_set_dneed<C>(B, S);
       pk_reload<C>(B, gl, rem, P);
     }
   } else {
@@ -520,7 +548,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
     if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
     else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
     if (ovf) {
-      pk_save<C>(B, G, gl, d, esc);
+      pk_save<C>(B, G, gl, d, esc, P);
       B.active = false;
       return;
     }
@@ -528,6 +556,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
       pk_shift1<C / 2>(B.E, G, gl, dir); pk_shift1<C / 2>(B.O, G, gl, dir);
       pk_rekey<C / 2>(B.E, pk_key_base(G, C, gl)); pk_rekey<C / 2>(B.O, pk_key_base(G, C, gl));
       B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
+      pk_set_dneed<C>(B, S);
       pk_reload<C>(B, gl, rem, P);
     }
   }
@@ -562,20 +591,19 @@ __device__ __forceinline__ void pk_chain_consts(const Band16<C>& B, uint32_t (&c
   }
 }
 
-// two anti-diagonals (d+1, d+2) and the block end; boundary masking only when some group needs it
+// two anti-diagonals (d+1, d+2) and the block end; the cells beyond the matrix are flagged (pk_beyond)
+// only when some lane's window can reach them (d + 2 > dneed), else the masks are 0
 template <int C, bool REDUX = true>
 __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int& rem, const Problem& P, int level,
                                         const Esc& esc, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
-  const int S = G * C;
   const int d2 = d + 2;
-  const bool need = B.active && (d2 - B.K0 - 2 * B.n > 0 || 2 * B.m - d2 - B.K0 < 2 * S - 1);
-  if (__any_sync(FULL, need)) {
-    pk_diag<C, 1, true, REDUX>(B, G, gl, d + 1, d + 1 - B.K0 - 2 * B.n, 2 * B.m - (d + 1) - B.K0, P, chc);
-    pk_diag<C, 0, true, REDUX>(B, G, gl, d2, d2 - B.K0 - 2 * B.n, 2 * B.m - d2 - B.K0, P, chc);
-  } else {
-    pk_diag<C, 1, false, REDUX>(B, G, gl, d + 1, 0, 0, P, chc);
-    pk_diag<C, 0, false, REDUX>(B, G, gl, d2, 0, 0, P, chc);
+  uint32_t by1 = 0, byr1 = 0, by2 = 0, byr2 = 0;
+  if (__any_sync(FULL, B.active && d2 > B.dneed)) {
+    pk_beyond<C>(B, gl, d + 1, 1, by1, byr1);
+    pk_beyond<C>(B, gl, d2, 0, by2, byr2);
   }
+  pk_diag<C, 1, REDUX>(B, G, gl, d + 1, by1, byr1, P, chc);
+  pk_diag<C, 0, REDUX>(B, G, gl, d2, by2, byr2, P, chc);
   d = d2;
   pk_block_end<C>(B, G, gl, d, rem, P, level, esc);
 }
@@ -583,16 +611,23 @@ __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int
 // tail stealing check (lane mode): once enough warps idle, checkpoint this lane's extension to
 // the steal queue if it still has >= min_rem anti-diagonals ahead
 template <int C>
-__device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st, const Esc& to) {
+__device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st, const Esc& to,
+                                         const Problem& P, const int* to_head = nullptr) {
   // (the group-uniform `left` test keeps pk_save's group shuffles converged for G > 1)
+  // to_head (endgame steals): steal only while idle warps outnumber the stolen records not yet
+  // claimed -- every stolen extension takes a whole warp, so stealing more than there are idle warps
+  // only moves extensions from 8-per-warp pools into a queue of one-per-warp units
   int go = 0;
-  if ((threadIdx.x & 31) == 0) go = ld_volatile(st.idle) >= st.thresh;
+  if ((threadIdx.x & 31) == 0) {
+    const int idle = ld_volatile(st.idle);
+    go = idle >= st.thresh && (to_head == nullptr || idle > ld_volatile(to.q_tail) - ld_volatile(to_head));
+  }
   go = __shfl_sync(FULL, go, 0);
   if (go && B.active) {
     const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
     const int left = 2 * min(B.m - ic, B.n - (d - ic));
     if (left >= st.min_rem) {
-      pk_save<C>(B, G, gl, d, to);
+      pk_save<C>(B, G, gl, d, to, P);
       B.active = false;
     }
   }
@@ -610,7 +645,7 @@ __device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, cons
     if ((++blk & 31) == 0) {
       pk_rebase<C>(B, d, P);
       if (G == 1 && st != nullptr) {
-        pk_steal<C>(B, G, gl, d, *st, st->es);
+        pk_steal<C>(B, G, gl, d, *st, st->es, P);
         if (!__any_sync(FULL, B.active)) break;
       }
     }
@@ -650,9 +685,10 @@ __device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int it
         if (u == u0) B.E[u] = h0 ? ((pk::DEAD2 & 0xffffu) | (v0 << 16)) : ((pk::DEAD2 & 0xffff0000u) | v0);
     }
   }
-  B.best = BIAS; B.istar = 0; B.jstar = 0; B.cells = 1; B.dbase = 0;
-  B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;
+  B.istar = 0; B.dstar = 0; B.cells = 1; B.dbase = 0;
+  B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;     // best = BIAS (pk_best)
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
+  pk_set_dneed<C>(B, S);
   if (B.active && B.m + B.n == 0) {
     if (gl == 0) {
       ExtOut o; o.best = 0; o.istar = 0; o.jstar = 0; o.level = 0; o.cells = 1; o.pad = 0;
@@ -694,8 +730,8 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
     d = rec[1];
     const int s_src = rec[14];
     const int sh = S - s_src;                            // K0' = K0 - sh (sh >= 0, even)
-    B.K0 = rec[2] - sh; B.dbase = rec[3]; B.thrN = rec[4]; B.best = rec[5];
-    B.istar = rec[6]; B.jstar = rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
+    B.K0 = rec[2] - sh; B.dbase = rec[3]; B.thrN = rec[4];      // rec[5] (best) follows from thrN
+    B.istar = rec[6]; B.dstar = rec[6] + rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
     B.maxL2 = rec[11]; B.ia0 = rec[12] - sh / 2; B.jb0 = rec[13] + sh / 2;
     B.cells = rec[15];
 #pragma unroll
@@ -705,8 +741,8 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
       w_o[t] = (qo >= 0 && qo < 2 * s_src) ? rec[HDR + qo] : NEGV;
     }
   } else {
-    B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1; B.dbase = 0; B.thrN = 0; B.best = 0;
-    B.istar = 0; B.jstar = 0; B.cells = 0; B.minL1 = EMIN; B.maxL1 = EMAX; B.minL2 = EMIN; B.maxL2 = EMAX;
+    B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1; B.dbase = 0; B.thrN = 0;
+    B.istar = 0; B.dstar = 0; B.cells = 0; B.minL1 = EMIN; B.maxL1 = EMAX; B.minL2 = EMIN; B.maxL2 = EMAX;
 #pragma unroll
     for (int t = 0; t < C; ++t) { w_e[t] = NEGV; w_o[t] = NEGV; }
   }
@@ -719,6 +755,7 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
   me = gmin_grp(me, G); mo = gmin_grp(mo, G);
   B.thrD = min(B.thrN + P.g, me);
   B.thrD1 = min(B.thrN + 2 * P.g, mo);
+  pk_set_dneed<C>(B, S);
   const int kb = pk_key_base(G, C, gl);
 #pragma unroll
   for (int u = 0; u < NP; ++u) {
@@ -832,7 +869,7 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
       // tail stealing: lane extensions to the 4-lane queue (tiers[0].src); endgame: a T1/T2 extension
       // with a long way to go leaves the wide C = 32 shape for the latency shape (32 lanes x 8 cells,
       // tiers[4].src) once enough warps idle.  One call site (pk_save is large)
-      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src);
+      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src, P, t == 0 ? nullptr : tiers[4].head);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above

@@ -75,3 +75,56 @@ def test_torchrun_reference_arm_two_ranks():
     assert d["impl"] == "reference" and d["unit"] == "GCUPS" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["ms_per_step"] > 0 and "sample_s" not in d["cpu_baseline"]
+
+
+def test_strong_shards_lpt_balance():
+    """bench.py --scaling strong: the same global batch split over ranks by the library's LPT on
+    estimated cells; shards are disjoint, cover every pair, and the LPT bound holds: the heaviest
+    shard exceeds the mean by at most the largest single item (PAPER.md:115-118 one2all splits a
+    batch over all GPUs; here by cost)."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import paper_2309_07270_b200 as xd
+    from synth import workload as W
+    w = W.config("cfg1")
+    cost = xd.pair_costs(w.offsets, w.pairs, w.k)
+    for n in (2, 3, 8):
+        sh = xd.shard_pairs(cost, n)
+        allidx = np.sort(np.concatenate(sh))
+        assert np.array_equal(allidx, np.arange(w.n_pairs))
+        loads = np.array([cost[s].sum() for s in sh])
+        assert loads.max() - loads.mean() <= cost.max()
+
+
+def _strong_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    class A:
+        config, scale, X, scaling = "tiny", 1.0, None, "strong"
+    w, idx = bench.rank_workload(A, rank, world)
+    out.put((rank, w.recipe["seed"], idx.tolist(), int(w.n_pairs)))
+    dist.destroy_process_group()
+
+
+def test_gloo_strong_scaling_shards():
+    """Under gloo with world_size 2, --scaling strong gives both ranks the SAME seeded batch and
+    disjoint LPT shards of it that together cover every pair."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_strong_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(2))
+    assert res[0][1] == res[1][1]                        # one global batch
+    a, b = set(res[0][2]), set(res[1][2])
+    assert not (a & b) and len(a | b) == res[0][3]

@@ -14,6 +14,8 @@ Both oracle implementations (C: oracle.extend, Python: xdrop_ref.extend) are
 pinned by the same checks, and must agree with each other.
 """
 import itertools
+
+import numpy as np
 import os
 import random
 
@@ -327,3 +329,79 @@ def test_rc_pairs_closed_form_and_equivalence():
     for t, (a, b, pa, pb) in enumerate(pairs_rc):         # and the Python twin
         p = ref.align(reads[a], reads[b & 0x7fffffff], pa, pb, 5, X=9, rc=True)
         assert (r1[t]["score"], r1[t]["b_begin"], r1[t]["b_end"], c1[t]) == (p["score"], p["b_begin"], p["b_end"], p["cells"])
+
+
+# ----------------------------------------------------------- f2 / f4 filter oracles (oracle/filters.py)
+def test_adaptive_keep_closed_form():
+    """Reading Q12 by hand: |A| = 100, |B| = 80, a_pos = 30, b_pos = 10 -> ov = min(30, 10) +
+    min(70, 70) = 80; phi = 0.5 -> mu = 40; c = 1.6 -> sqrt(64) = 8 -> threshold 32 (exact in
+    binary), so score 32 is kept and 31 is not; c = 0 -> the threshold is mu itself; c = 1e9 puts it
+    at 40 - 2e5, below every score here."""
+    from oracle import filters as F
+    off = np.array([0, 100, 180], dtype=np.int64)
+    pairs = np.array([[0, 1, 30, 10]] * 4, dtype=np.int32)
+    assert F.overlap_estimate(off, off, pairs[0]) == 80
+    assert list(F.adaptive_keep(off, off, pairs, [32, 31, 40, 39], 0.5, 1.6)) == [1, 0, 1, 1]
+    assert list(F.adaptive_keep(off, off, pairs, [40, 39, 41, 0], 0.5, 0.0)) == [1, 0, 1, 0]
+    assert list(F.adaptive_keep(off, off, pairs, [0, 1, 5, -1], 0.5, 1e9)) == [1, 1, 1, 1]   # t = 40 - 2e5 < -1
+    # the RC bit of b_id does not change B's length; seeds at the read ends give ov = the other side
+    rc = np.array([[0, 1 | -(1 << 31), 0, 0], [0, 1, 100, 80]], dtype=np.int32)
+    assert F.overlap_estimate(off, off, rc[0]) == 80 and F.overlap_estimate(off, off, rc[1]) == 80
+
+
+def test_adaptive_keep_monotone():
+    """keep is monotone in the score and antitone in phi (for c fixed), at any size."""
+    from oracle import filters as F
+    rng = np.random.default_rng(3)
+    off = np.concatenate([[0], np.cumsum(rng.integers(200, 2000, size=20))]).astype(np.int64)
+    L = np.diff(off)
+    n = 300
+    a = rng.integers(0, 20, size=n); b = rng.integers(0, 20, size=n)
+    pairs = np.stack([a, b, (rng.random(n) * (L[a] - 17)).astype(int), (rng.random(n) * (L[b] - 17)).astype(int)],
+                     axis=1).astype(np.int32)
+    s = rng.integers(-50, 2000, size=n)
+    k1 = F.adaptive_keep(off, off, pairs, s, 0.3, 8.0)
+    assert np.all(F.adaptive_keep(off, off, pairs, s + 1, 0.3, 8.0) >= k1)
+    assert np.all(F.adaptive_keep(off, off, pairs, s, 0.4, 8.0) <= k1)
+
+
+def test_seed_kmer_freq_hand_cases():
+    """Canonical k-mer counts by hand.  Pool ["AAAA", "TTTT", "ACG", "TAC", "ANAC"], k = 3:
+    AAA occurs twice in read 0 and its reverse complement TTT twice in read 1 -> 4; ACG (its
+    reverse complement CGT) occurs once in read 2 -- the CGT across the read-2/read-3 boundary does
+    not count; TAC (canonical GTA) once in read 3; the 3-mers of read 4 with N do not count, NAC
+    neither, so nothing else is added."""
+    from oracle import filters as F
+    reads = ["AAAA", "TTTT", "ACG", "TAC", "ANAC"]
+    seq = np.frombuffer("".join(reads).encode(), dtype=np.uint8)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in reads])]).astype(np.int64)
+    pairs = np.array([[0, 1, 0, 0], [1, 0, 1, 0], [2, 0, 0, 0], [3, 0, 0, 0]], dtype=np.int32)
+    freq, keep = F.seed_kmer_freq(seq, off, pairs, 3, 2, 4)
+    assert list(freq) == [4, 4, 1, 1] and list(keep) == [1, 1, 0, 0]
+    assert F.canonical("ACG") == "ACG" and F.canonical("CGT") == "ACG" and F.canonical("TAC") == "GTA"
+    assert F.canonical("ANA") is None
+    counts = F.kmer_counts(seq, off, 3)
+    assert counts == {"AAA": 4, "ACG": 1, "GTA": 1}
+
+
+def test_seed_kmer_freq_invariants():
+    """Every valid seed occurs at least once (itself); a seed and its reverse complement planted in
+    another read have the same count; the counts sum to the number of ACGT k-mer positions."""
+    from oracle import filters as F
+    rng = np.random.default_rng(11)
+    reads = ["".join(rng.choice(list("ACGT"), size=int(rng.integers(5, 60)))) for _ in range(30)]
+    seq = np.frombuffer("".join(reads).encode(), dtype=np.uint8)
+    off = np.concatenate([[0], np.cumsum([len(r) for r in reads])]).astype(np.int64)
+    k = 4
+    pairs = np.array([[r, 0, int(rng.integers(0, len(reads[r]) - k + 1)), 0] for r in range(30)], dtype=np.int32)
+    freq, _ = F.seed_kmer_freq(seq, off, pairs, k, 0, 10 ** 9)
+    assert np.all(freq >= 1)
+    assert sum(F.kmer_counts(seq, off, k).values()) == sum(max(0, len(r) - k + 1) for r in reads)
+    km = reads[0][:k]
+    rcs = "".join({"A": "T", "C": "G", "G": "C", "T": "A"}[c] for c in reversed(km))
+    reads2 = reads + [rcs]
+    seq2 = np.frombuffer("".join(reads2).encode(), dtype=np.uint8)
+    off2 = np.concatenate([[0], np.cumsum([len(r) for r in reads2])]).astype(np.int64)
+    f0, _ = F.seed_kmer_freq(seq, off, np.array([[0, 0, 0, 0]], dtype=np.int32), k, 0, 99)
+    f1, _ = F.seed_kmer_freq(seq2, off2, np.array([[0, 0, 0, 0], [30, 0, 0, 0]], dtype=np.int32), k, 0, 99)
+    assert f1[0] == f1[1] == f0[0] + 1

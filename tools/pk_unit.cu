@@ -22,15 +22,15 @@ __global__ void unit(Problem P, int* nbad, int* out) {
     B.A0 = rnd(seed); B.A1 = rnd(seed); B.B0 = rnd(seed); B.B1 = rnd(seed);
     B.thrD1 = 1000; B.thrD = B.thrD1 + 1 + rnd(seed) % 3; B.thrN = B.thrD + 1 + rnd(seed) % 3;
     Band16<32> B2 = B;
-    const int qlo = (int)(rnd(seed) % 80) - 8, qhi = qlo + (int)(rnd(seed) % 80);
+    const uint32_t by = (rnd(seed) & 1) ? 0u : rnd(seed);     // cells beyond the matrix (pk_beyond)
     uint32_t ch1[2], ch2[2];
     uint32_t k1, k2;
     if (PAR == 0) {
-      k1 = pk_cells<32, 0, true, false>(B.E, B.O, B, 1, 0, qlo, qhi, P, ch1);
-      k2 = pk_cells<32, 0, true, true>(B2.E, B2.O, B2, 1, 0, qlo, qhi, P, ch2);
+      k1 = pk_cells<32, 0, false>(B.E, B.O, B, 1, 0, by, P, ch1);
+      k2 = pk_cells<32, 0, true>(B2.E, B2.O, B2, 1, 0, by, P, ch2);
     } else {
-      k1 = pk_cells<32, 1, true, false>(B.O, B.E, B, 1, 0, qlo, qhi, P, ch1);
-      k2 = pk_cells<32, 1, true, true>(B2.O, B2.E, B2, 1, 0, qlo, qhi, P, ch2);
+      k1 = pk_cells<32, 1, false>(B.O, B.E, B, 1, 0, by, P, ch1);
+      k2 = pk_cells<32, 1, true>(B2.O, B2.E, B2, 1, 0, by, P, ch2);
     }
     bool bad = k1 != k2 || ch1[0] != ch2[0] || ch1[1] != ch2[1];
     for (int u = 0; u < 16; ++u) bad |= (B.E[u] != B2.E[u]) || (B.O[u] != B2.O[u]);

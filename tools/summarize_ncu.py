@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STEP_KERNELS = ("pk_tiered_kernel", "pk_merged_kernel", "pk_resume_kernel", "band_cta_kernel", "band_merged_kernel", "band_kernel", "general_kernel", "pack_kernel", "prep_kernel",
+STEP_KERNELS = ("pk_tiered_kernel", "pk_merged_kernel", "pk_probe_kernel", "pk_resume_kernel", "band_cta_kernel", "band_merged_kernel", "band_kernel", "general_kernel", "pack_kernel", "prep_kernel",
                 "scan_kernel", "scatter_kernel", "combine_kernel", "init_bad_kernel", "init_counters_kernel")
 
 
