@@ -272,6 +272,13 @@ int64_t xdrop_last_timeline(const xdrop_ctx* ctx, uint64_t* buf, int64_t cap);
  * batch <= counts[r]; -1 when the walk returns to `rank`. */
 int xdrop_ring_left(int rank, int batch, const int* counts, int n);
 int xdrop_ring_right(int rank, int batch, const int* counts, int n);
+/* Reading Q21's token order over one ring of n members (member v has counts[v] batches, each of
+ * turns_per_batch turns): the member index owning the turn after (batch b, iteration it) of member u,
+ * with that turn's batch / iteration in *next_b / *next_it (nullable), or -1 if none; _prev: the member
+ * owning the turn before, or -1.  The scheduler and the multi-process rank mode both use these. */
+int xdrop_ring_turn_next(int u, int b, int it, const int* counts, int n, int turns_per_batch,
+                         int* next_b, int* next_it);
+int xdrop_ring_turn_prev(int u, int b, int it, const int* counts, int n, int turns_per_batch);
 
 int xdrop_finalize(xdrop_ctx* ctx);
 const char* xdrop_strerror(int status);

@@ -69,7 +69,7 @@ EXPORTS = [
     "xdrop_last_sched_stats", "xdrop_last_trace", "xdrop_sched_simulate", "xdrop_ring_left",
     "xdrop_ring_right", "xdrop_finalize", "xdrop_strerror", "xdrop_last_error_index", "xdrop_alu_peaks",
     "xdrop_last_timeline", "xdrop_pool_register", "xdrop_align_pooled", "xdrop_pool_release",
-    "xdrop_adaptive_filter_device", "xdrop_seed_kmer_freq_device",
+    "xdrop_adaptive_filter_device", "xdrop_seed_kmer_freq_device", "xdrop_ring_turn_next", "xdrop_ring_turn_prev",
 ]
 
 
@@ -97,6 +97,8 @@ def _load():
     lib.xdrop_sched_simulate.restype = ctypes.c_int64
     lib.xdrop_ring_left.argtypes = [ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
     lib.xdrop_ring_right.argtypes = [ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
+    lib.xdrop_ring_turn_next.argtypes = [ctypes.c_int] * 3 + [P, ctypes.c_int, ctypes.c_int, P, P]
+    lib.xdrop_ring_turn_prev.argtypes = [ctypes.c_int] * 3 + [P, ctypes.c_int, ctypes.c_int]
     lib.xdrop_finalize.argtypes = [P]
     lib.xdrop_strerror.argtypes = [ctypes.c_int]
     lib.xdrop_strerror.restype = ctypes.c_char_p

@@ -285,6 +285,33 @@ extern "C" int xdrop_ring_right(int rank, int batch, const int* counts, int n) {
   return xdrop_right_successor(rank, batch, counts, n);
 }
 
+// Reading Q21's token order over one ring (members 0..n-1 with counts[v] batches each, turns_per_batch
+// turns per batch): the member owning the turn after / before (batch b, iteration it) of member u.
+// Exported so that the multi-process rank mode (ranks.py) uses this one implementation.
+extern "C" int xdrop_ring_turn_next(int u, int b, int it, const int* counts, int n, int turns_per_batch,
+                                    int* next_b, int* next_it) {
+  if (!counts || n < 1 || u < 0 || u >= n || turns_per_batch < 1) return -1;
+  Ring r;
+  r.members.resize((size_t)n);
+  for (int v = 0; v < n; ++v) r.members[(size_t)v] = v;
+  r.counts.assign(counts, counts + n);
+  r.turns_per_batch = turns_per_batch;
+  int nb = 0, nit = 0;
+  const int v = r.next(u, b, it, nb, nit);
+  if (next_b) *next_b = nb;
+  if (next_it) *next_it = nit;
+  return v;
+}
+extern "C" int xdrop_ring_turn_prev(int u, int b, int it, const int* counts, int n, int turns_per_batch) {
+  if (!counts || n < 1 || u < 0 || u >= n || turns_per_batch < 1) return -1;
+  Ring r;
+  r.members.resize((size_t)n);
+  for (int v = 0; v < n; ++v) r.members[(size_t)v] = v;
+  r.counts.assign(counts, counts + n);
+  r.turns_per_batch = turns_per_batch;
+  return r.prev(u, b, it);
+}
+
 extern "C" int64_t xdrop_sched_simulate(int m, int policy, int n_ranks, int batch_size, int subbatches,
                                         const int64_t* w, int64_t n, double ns_per_unit, xdrop_sched_stats* st,
                                         xdrop_trace_event* trace, int64_t cap, int32_t* gpu_of_pair) {

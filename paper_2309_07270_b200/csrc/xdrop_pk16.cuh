@@ -612,16 +612,10 @@ __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int
 // the steal queue if it still has >= min_rem anti-diagonals ahead
 template <int C>
 __device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st, const Esc& to,
-                                         const Problem& P, const int* to_head = nullptr) {
+                                         const Problem& P) {
   // (the group-uniform `left` test keeps pk_save's group shuffles converged for G > 1)
-  // to_head (endgame steals): steal only while idle warps outnumber the stolen records not yet
-  // claimed -- every stolen extension takes a whole warp, so stealing more than there are idle warps
-  // only moves extensions from 8-per-warp pools into a queue of one-per-warp units
   int go = 0;
-  if ((threadIdx.x & 31) == 0) {
-    const int idle = ld_volatile(st.idle);
-    go = idle >= st.thresh && (to_head == nullptr || idle > ld_volatile(to.q_tail) - ld_volatile(to_head));
-  }
+  if ((threadIdx.x & 31) == 0) go = ld_volatile(st.idle) >= st.thresh;
   go = __shfl_sync(FULL, go, 0);
   if (go && B.active) {
     const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
@@ -869,7 +863,7 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
       // tail stealing: lane extensions to the 4-lane queue (tiers[0].src); endgame: a T1/T2 extension
       // with a long way to go leaves the wide C = 32 shape for the latency shape (32 lanes x 8 cells,
       // tiers[4].src) once enough warps idle.  One call site (pk_save is large)
-      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src, P, t == 0 ? nullptr : tiers[4].head);
+      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src, P);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above

@@ -55,30 +55,25 @@ def subbatches(lo: int, hi: int, batch_size: int, c: int) -> list[list[np.ndarra
 # ----------------------------------------------------------------- token order
 @dataclass
 class Ring:
+    """Reading Q21's token order over one ring; the order itself is the C library's
+    (xdrop_ring_turn_next / _prev, csrc/sched.cpp), the one the in-process scheduler uses."""
     members: list[int]          # rank ids, ascending
     counts: list[int]           # batches per member
     turns_per_batch: int        # c (per sub-batch token) or 1 (per batch token)
 
-    def _first(self, b):
-        return next((v for v in range(len(self.members)) if self.counts[v] >= b), -1)
-
-    def _last(self, b):
-        return next((v for v in range(len(self.members) - 1, -1, -1) if self.counts[v] >= b), -1)
+    def _counts(self):
+        import ctypes
+        return (ctypes.c_int * len(self.counts))(*[int(x) for x in self.counts])
 
     def next(self, u: int, b: int, it: int) -> int:
         """Member index owning the turn after (b, it, u); -1 if none (reading Q21)."""
-        for v in range(u + 1, len(self.members)):
-            if self.counts[v] >= b:
-                return v
-        bb, ii = (b, it + 1) if it < self.turns_per_batch else (b + 1, 1)
-        return self._first(bb)
+        from . import _native as N
+        return int(N.lib.xdrop_ring_turn_next(u, b, it, self._counts(), len(self.counts), self.turns_per_batch,
+                                              None, None))
 
     def prev(self, u: int, b: int, it: int) -> int:
-        for v in range(u - 1, -1, -1):
-            if self.counts[v] >= b:
-                return v
-        bb, ii = (b, it - 1) if it > 1 else (b - 1, self.turns_per_batch)
-        return self._last(bb) if bb >= 1 else -1
+        from . import _native as N
+        return int(N.lib.xdrop_ring_turn_prev(u, b, it, self._counts(), len(self.counts), self.turns_per_batch))
 
 
 def ring_of(policy: str, rank: int, n_ranks: int, m: int) -> list[int]:

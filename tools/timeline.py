@@ -31,7 +31,14 @@ edges = np.linspace(0, T, 21)
 for a, b in zip(edges[:-1], edges[1:]):
     lo, hi = t0 + a * 1e6, t0 + b * 1e6
     busy = ((np.minimum(tl[:, 3], hi) - np.maximum(tl[:, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
-    print(f"  [{a:5.1f},{b:5.1f}) ms busy warps {busy*100:5.1f}%")
+    per = []
+    for ty in range(8):
+        m = tl[:, 0] == ty
+        if m.any():
+            bt = ((np.minimum(tl[m, 3], hi) - np.maximum(tl[m, 2], lo)).clip(0)).sum() / ((hi - lo) * nw)
+            if bt > 0.005:
+                per.append(f"{names[ty]} {bt*100:4.1f}")
+    print(f"  [{a:5.1f},{b:5.1f}) ms busy warps {busy*100:5.1f}%   " + ", ".join(per))
 # the latest-ending work units
 if len(sys.argv) > 2:
     o = np.argsort(-tl[:, 3])[:int(sys.argv[2])]
