@@ -93,6 +93,35 @@ def allgather(x: float, world: int, device=None) -> list:
     return [float(o.item()) for o in out]
 
 
+def gather_results(out, cells, idx, n_total, world, device=None):
+    """--scaling strong: the optional result gather of SURVEY.md §8(e) (24 B per pair over NCCL, or gloo
+    on CPU).  Every rank contributes its shard's (n, 5) int32 results and int64 cells at the pair
+    indices `idx` it aligned; returns the global (n_total, 5) / (n_total,) arrays on every rank."""
+    import torch
+    if world == 1:
+        return out, cells
+    import torch.distributed as dist
+    n_my = torch.tensor([int(idx.shape[0])], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n_my) for _ in range(world)]
+    dist.all_gather(sizes, n_my)
+    cap = int(max(int(x.item()) for x in sizes))
+    pad = torch.full((cap, 7), -1, dtype=torch.int64, device=device)
+    k = int(idx.shape[0])
+    if k:
+        pad[:k, 0] = torch.as_tensor(idx, dtype=torch.int64, device=device)
+        pad[:k, 1:6] = out.to(device=device, dtype=torch.int64)
+        pad[:k, 6] = cells.to(device=device, dtype=torch.int64)
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    full = torch.cat(parts, 0)
+    full = full[full[:, 0] >= 0]
+    g_out = torch.zeros((n_total, 5), dtype=torch.int32, device=device)
+    g_cells = torch.zeros(n_total, dtype=torch.int64, device=device)
+    g_out[full[:, 0]] = full[:, 1:6].to(torch.int32)
+    g_cells[full[:, 0]] = full[:, 6]
+    return g_out, g_cells
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -459,9 +488,14 @@ def run_native(args, world, rank, local):
     # checked against it pair by pair (parity of the number this line reports)
     cpu = None
     parity = None
+    chk_w = w.subset(sidx) if n_my != w.n_pairs else w
+    if args.scaling == "strong" and world > 1:
+        # results of the whole global batch on every rank (untimed): rank 0's parity check below
+        # then covers pairs of every shard
+        out_d, cells_d = gather_results(out_d, cells_d, sidx, w.n_pairs, world, dev)
+        chk_w = w
     if rank == 0 and not args.no_cpu:
-        base, (idx, ref, rcells) = oracle_sample(w.subset(sidx) if n_my != w.n_pairs else w,
-                                                 args.cpu_seconds if world == 1 else 2.0)
+        base, (idx, ref, rcells) = oracle_sample(chk_w, args.cpu_seconds if world == 1 else 2.0)
         if world == 1:
             cpu = {k: x for k, x in base.items() if k not in ("sample_s", "sample_pairs")}
         o = out_d.cpu().numpy()[idx]

@@ -128,3 +128,41 @@ def test_gloo_strong_scaling_shards():
     assert res[0][1] == res[1][1]                        # one global batch
     a, b = set(res[0][2]), set(res[1][2])
     assert not (a & b) and len(a | b) == res[0][3]
+
+
+def _gather_worker(rank, world, port, out):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 11
+    idx = np.arange(rank, n, world)                      # disjoint shards of a global batch
+    res = torch.from_numpy(np.stack([idx * 10 + j for j in range(5)], axis=1).astype(np.int32))
+    cells = torch.from_numpy((idx * 1000).astype(np.int64))
+    g, c = bench.gather_results(res, cells, idx, n, world)
+    out.put((rank, g.numpy().tolist(), c.numpy().tolist()))
+    dist.destroy_process_group()
+
+
+def test_gloo_strong_result_gather():
+    """--scaling strong's result gather (optional): every rank ends with the whole
+    batch's results in pair order, shards of unequal size included."""
+    import numpy as np
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(3))
+    want = [[10 * i + j for j in range(5)] for i in range(11)]
+    for _, g, c in res:
+        assert g == want and c == [1000 * i for i in range(11)]
