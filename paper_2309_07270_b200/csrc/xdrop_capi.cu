@@ -225,14 +225,12 @@ int64_t packed_words(int64_t len) { return (len + 2 * xk::GUARD + 15) / 16 + 2; 
 int pack_pool(DevCtx& D, const char* d_seq, int64_t len, Buf& out, cudaStream_t s, int64_t& launches) {
   const int64_t nw = packed_words(len);
   CKR(out.ensure((size_t)nw * 4));
-  CK(cudaMemsetAsync(out.p, 0, (size_t)nw * 4, s));
-  const int64_t work = (len + xk::GUARD + 15) / 16;
+  // the kernel writes every word of the packed pool (the guard bands as 0): no memset
   const int thr = 256;
-  if (work > 0) {
-    xk::pack_kernel<<<(unsigned)((work + thr - 1) / thr), thr, 0, s>>>(d_seq, len, out.as<uint32_t>(),
+  const int64_t threads = (nw + 3) / 4;
+  xk::pack_kernel<<<(unsigned)((threads + thr - 1) / thr), thr, 0, s>>>(d_seq, len, out.as<uint32_t>(), nw,
                                                                       D.bad.as<unsigned long long>());
-    ++launches;
-  }
+  ++launches;
   return cuda_err(cudaGetLastError());
 }
 

@@ -1535,26 +1535,54 @@ __device__ __forceinline__ uint32_t code_of(unsigned ch, int64_t t, unsigned lon
   if (!(u == 'A' || u == 'C' || u == 'G' || u == 'T')) atomicMin(bad, (unsigned long long)t);
   return ((ch >> 1) ^ (ch >> 2)) & 3u;   // A/a 0, C/c 1, G/g 2, T/t 3
 }
-__global__ void pack_kernel(const char* __restrict__ seq, int64_t len, uint32_t* __restrict__ out,
-                            unsigned long long* bad) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // output word of the pool
-  const int64_t nwords = (len + GUARD + 15) / 16;
-  if (w >= nwords) return;
-  uint32_t word = 0;
-  const int64_t t0 = w * 16 - GUARD;   // pool index of the first base in this word (GUARD % 16 == 0)
-  if (t0 >= 0 && t0 + 16 <= len && ((reinterpret_cast<uintptr_t>(seq) & 15) == 0)) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(seq + t0));   // one 16-byte load
-    const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+// 16 ASCII bases (one aligned uint4) -> one 2-bit word, four bases per 32-bit SIMD step:
+// ((c >> 1) ^ (c >> 2)) & 3 is A0 C1 G2 T3 (either case) for each byte at once; returns false if any
+// byte is outside {A,C,G,T,a,c,g,t}
+__device__ __forceinline__ bool pack16(const uint4 q, uint32_t& word) {
+  const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+  uint32_t ok = 0xffffffffu;
+  word = 0;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) word |= code_of((v[u >> 2] >> (8 * (u & 3))) & 0xFFu, t0 + u, bad) << (2 * u);
-  } else {
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int64_t t = t0 + u;
-      if (t >= 0 && t < len) word |= code_of((unsigned char)seq[t], t, bad) << (2 * u);
-    }
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t u = v[k] & 0xDFDFDFDFu;          // upper case
+    ok &= __vcmpeq4(u, 0x41414141u) | __vcmpeq4(u, 0x43434343u) | __vcmpeq4(u, 0x47474747u) |
+          __vcmpeq4(u, 0x54545454u);
+    const uint32_t c = ((v[k] >> 1) ^ (v[k] >> 2)) & 0x03030303u;
+    word |= ((c | (c >> 6) | (c >> 12) | (c >> 18)) & 0xFFu) << (8 * k);
   }
-  out[w] = word;
+  return ok == 0xffffffffu;
+}
+// Every word of the packed pool (guards included: their bases are 0), four words per thread from four
+// 16-byte loads when the ASCII pool is 16-byte aligned and the words are inside it; the per-byte path
+// handles the pool's ends and records the index of a bad base.
+__global__ void pack_kernel(const char* __restrict__ seq, int64_t len, uint32_t* __restrict__ out,
+                            int64_t nwords, unsigned long long* bad) {
+  const int64_t w0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);   // first output word
+  if (w0 >= nwords) return;
+  const bool al = (reinterpret_cast<uintptr_t>(seq) & 15) == 0;
+  uint32_t words[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t w = w0 + k;
+    const int64_t t0 = w * 16 - GUARD;   // pool index of the first base in this word (GUARD % 16 == 0)
+    uint32_t word = 0;
+    bool done = false;
+    if (al && t0 >= 0 && t0 + 16 <= len) done = pack16(__ldg(reinterpret_cast<const uint4*>(seq + t0)), word);
+    if (!done && w < nwords) {
+      word = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int64_t t = t0 + u;
+        if (t >= 0 && t < len) word |= code_of((unsigned char)seq[t], t, bad) << (2 * u);
+      }
+    }
+    words[k] = word;
+  }
+  if (w0 + 4 <= nwords) {
+    *reinterpret_cast<uint4*>(out + w0) = make_uint4(words[0], words[1], words[2], words[3]);
+  } else {
+    for (int k = 0; k < 4 && w0 + k < nwords; ++k) out[w0 + k] = words[k];
+  }
 }
 
 // validate pairs, estimate costs, histogram of cost buckets.  A pair is valid when its read ids are

@@ -87,3 +87,16 @@ def test_ecoli_every_pair_host_api(xd, ecoli):
     with xd.Aligner() as al:
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
     assert_same(res, cells, ref, rcells, "ecoli all pairs, host API")
+
+
+@pytest.mark.parametrize("policy,c", [("one2all", 1), ("one2one", 1), ("opt_one2one", 1), ("one2one", 4)])
+def test_ecoli_every_pair_paper_policies(xd, ecoli, policy, c):
+    """BASELINE configs[2]: the same E. coli-shaped batch under the paper's policies with its 16 ranks
+    (PAPER.md:277), batches of 10,000 and c sub-batches, on four logical devices
+    (streams of the one B200 here): every pair bit-exact, whatever the policy."""
+    w, ref, rcells = ecoli
+    with xd.Aligner(devices=[0, 0, 0, 0], policy=policy, n_ranks=16, batch_size=10000, subbatches=c) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+        st = al.stats()
+    assert_same(res, cells, ref, rcells, f"ecoli {policy} c={c}")
+    assert st["cells"] == int(rcells.sum())
