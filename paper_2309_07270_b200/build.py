@@ -11,7 +11,7 @@ OUT = os.path.join(HERE, "libxdrop.so")
 # tests only: the same sources with -DXDROP_CHECKED (every packed-pool read bounds-checked, traps)
 OUT_CHECKED = os.path.join(HERE, "libxdrop_checked.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("xdrop_capi.cu", "xdrop_peaks.cu", "xdrop_filters.cu", "sched.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("xdrop_kernels.cuh", "xdrop_pk16.cuh", "sched.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("xdrop_kernels.cuh", "xdrop_pk16.cuh", "xdrop_pkwide.cuh", "sched.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "xdrop.h")]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared"]

@@ -98,8 +98,9 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
+  int wide_pk = 1;            // S = 2048 level in the packed 2-warp kernel (XDROP_WIDE_PK=0: 32-bit CTA)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
                               // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
   int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
@@ -197,6 +198,9 @@ int dev_open(DevCtx& D, int dev) {
   D.occ_cta = std::max(1, D.occ_cta);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta1k, xk::band_cta_kernel<128, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta2k, xk::band_cta_kernel<128, 16>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkw, xk::pk_wide_kernel, 64, 0));
+  D.occ_pkw = std::max(1, D.occ_pkw);
+  if (const char* e = getenv("XDROP_WIDE_PK")) D.wide_pk = atoi(e);
   D.occ_cta2k = std::max(1, D.occ_cta2k);
   D.occ_cta1k = std::max(1, D.occ_cta1k);
   if (const char* e = getenv("XDROP_SHARED_T3")) D.shared_t3 = atoi(e);
@@ -469,7 +473,10 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         xk::band_resume_kernel<32, 32><<<D.sms * D.occ_l2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
       // CTA levels: S = 2048 (4 warps x 32 lanes x 16 cells; twice the resident extensions of the
       // 8-warp block) checkpointing its overflows for S = 4096 (8 warps x 32 x 16)
-      xk::band_cta_kernel<128, 16><<<D.sms * D.occ_cta2k, 128, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
+      if (pk && D.wide_pk)        // packed S = 2048: one extension per 2-warp block (xdrop_pkwide.cuh)
+        xk::pk_wide_kernel<<<D.sms * D.occ_pkw, 64, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
+      else
+        xk::band_cta_kernel<128, 16><<<D.sms * D.occ_cta2k, 128, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
       xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e5, ctr + C_HEAD5, eg, 2);
       launches += 3;
     }

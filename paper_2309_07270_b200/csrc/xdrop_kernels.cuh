@@ -734,6 +734,7 @@ __device__ __forceinline__ int wait_entry_w(const int* q, int h, int lane) {
 }
 
 #include "xdrop_pk16.cuh"
+#include "xdrop_pkwide.cuh"
 
 // Standalone kernel resuming checkpointed extensions in the packed 16-bit mode (X + M <= 510).
 #ifndef XDROP_PKR_MINBLOCKS

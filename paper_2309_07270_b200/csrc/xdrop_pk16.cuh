@@ -196,10 +196,12 @@ __device__ __forceinline__ uint32_t tree16(const uint32_t (&k)[N]) {
 // N (holds d-1).  by: local cells (bit tl) beyond the matrix (i > m or j > n; 0 away from the
 // edges): they compare as mismatches, so their values only fall along any path (pk_diag shows why
 // they then never matter).  Returns the lane's packed key maximum; ch[] are the PRMT-mask chains.
-template <int C, int PAR, bool FMA = (XDROP_PK_FMA != 0)>
+// XW (pk_wide_kernel, G = 64 lanes over two warps): the seam of the warp's boundary lane comes from
+// the other warp through shared memory (xseam; DEAD2 at the group's own edges)
+template <int C, int PAR, bool FMA = (XDROP_PK_FMA != 0), bool XW = false>
 __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_t (&N)[C / 2], const Band16<C>& B,
                                              int G, int gl, uint32_t by, const Problem& P,
-                                             uint32_t (&ch)[C > 16 ? 2 : 1]) {
+                                             uint32_t (&ch)[C > 16 ? 2 : 1], uint32_t xseam = 0) {
   constexpr int NP = C / 2, NCH = C > 16 ? 2 : 1, NPC = NP / NCH;
   const int thr_d = B.thrN;
   const uint32_t two = (uint32_t)P.keym >> (KEYSH - 1);  // 2, opaque: keeps the chains on IMAD
@@ -227,11 +229,13 @@ __device__ __forceinline__ uint32_t pk_cells(uint32_t (&V)[C / 2], const uint32_
   uint32_t seam;
   if constexpr (PAR == 0) {
     uint32_t x = pk::DEAD2;
-    if (G > 1) { x = __shfl_up_sync(FULL, N[NP - 1], 1, G); if (gl == 0) x = pk::DEAD2; }
+    if constexpr (XW) { x = __shfl_up_sync(FULL, N[NP - 1], 1); if ((gl & 31) == 0) x = xseam; }
+    else if (G > 1) { x = __shfl_up_sync(FULL, N[NP - 1], 1, G); if (gl == 0) x = pk::DEAD2; }
     seam = __byte_perm(N[NP - 1], x, 0x1076);            // (left lane's last odd cell, own odd cell NP-1)
   } else {
     uint32_t x = pk::DEAD2;
-    if (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
+    if constexpr (XW) { x = __shfl_down_sync(FULL, N[0], 1); if ((gl & 31) == 31) x = xseam; }
+    else if (G > 1) { x = __shfl_down_sync(FULL, N[0], 1, G); if (gl == G - 1) x = pk::DEAD2; }
     seam = __byte_perm(N[0], x, 0x5432);                 // (own even cell NP, right lane's even cell 0)
   }
   // the hi half of a seam pair may hold a cell with key bits up to 31 (the next lane's cell 0);
