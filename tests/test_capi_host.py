@@ -158,3 +158,32 @@ def test_peak_probes_sass(tmp_path):
         if m.group(1) == "5":
             assert abs(c["IMAD"] - c["VIMNMX3.S16x2"]) <= 0.05 * named, c
     assert seen == set(want), seen
+
+
+def test_new_entry_points_argument_errors(xd):
+    """Argument checks of the round-2 entry points that need no GPU: bad sizes / parameters return
+    XDROP_EINVAL before any CUDA call (include/xdrop.h)."""
+    import ctypes
+    from paper_2309_07270_b200 import _native as N
+    out = (ctypes.c_double * 4)()
+    assert N.lib.xdrop_alu_peaks(0, out, 4) == N.EINVAL                      # n_out < 12
+    assert N.lib.xdrop_alu_peaks(0, None, 12) == N.EINVAL
+    err = ctypes.c_int64(7)
+    # adaptive filter: phi must be > 0, c >= 0; n < 0 invalid; n == 0 is a no-op
+    assert N.lib.xdrop_adaptive_filter_device(None, 0, None, 0, None, None, 0, 0.0, 1.0, None,
+                                              ctypes.byref(err), None) == N.EINVAL
+    assert N.lib.xdrop_adaptive_filter_device(None, 0, None, 0, None, None, -1, 0.5, 1.0, None, None, None) == N.EINVAL
+    assert N.lib.xdrop_adaptive_filter_device(None, 0, None, 0, None, None, 0, 0.5, 1.0, None,
+                                              ctypes.byref(err), None) == N.OK
+    assert err.value == -1
+    # k-mer band: 1 <= k <= 31; n == 0 is a no-op; a NULL pointer with n > 0 is invalid
+    assert N.lib.xdrop_seed_kmer_freq_device(None, None, 0, 0, None, 0, 32, 0, 1, None, None, None, None) == N.EINVAL
+    assert N.lib.xdrop_seed_kmer_freq_device(None, None, 0, 0, None, 0, 17, 0, 1, None, None, None, None) == N.OK
+    assert N.lib.xdrop_seed_kmer_freq_device(None, None, 0, 0, None, 5, 17, 0, 1, None, None, None, None) == N.EINVAL
+    # ring order helpers: a consistent next / prev walk over a skewed ring (reading Q21)
+    counts = (ctypes.c_int * 3)(2, 2, 1)
+    nb, nit = ctypes.c_int(0), ctypes.c_int(0)
+    assert N.lib.xdrop_ring_turn_next(2, 1, 1, counts, 3, 1, ctypes.byref(nb), ctypes.byref(nit)) == 0
+    assert (nb.value, nit.value) == (2, 1)                                 # batch 2 of member 0
+    assert N.lib.xdrop_ring_turn_prev(0, 2, 1, counts, 3, 1) == 2
+    assert N.lib.xdrop_ring_turn_next(1, 2, 1, counts, 3, 1, None, None) == -1

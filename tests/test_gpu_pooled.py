@@ -71,3 +71,26 @@ def test_pooled_two_pools_and_errors(xd):
         assert e.value.status == -4 and e.value.index == 5
         res2, _ = al.align_pooled(pa, w.pairs, k=w.k, X=w.X)   # still usable after the errors
         assert np.array_equal(res2, ref)
+
+
+def test_pooled_edge_cases(xd):
+    """Empty batches and pools with empty reads; k-mer band and adaptive filter on empty inputs."""
+    import torch
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=93, n_pairs=40, len_lo=0, len_hi=400, k=9, X=10)
+    ref, rcells = oracle_of(w)
+    with xd.Aligner() as al:
+        pid = al.register_pool(w.seq, w.offsets)
+        res, cells = al.align_pooled(pid, w.pairs[:0], k=w.k, X=w.X)
+        assert res.shape == (0,) and cells.shape == (0,)
+        res, cells = al.align_pooled(pid, w.pairs, k=w.k, X=w.X)
+        assert_same(res, cells, ref, rcells, "pool with empty reads")
+        empty = al.register_pool(np.zeros(0, np.uint8), np.zeros(1, np.int64))
+        res, _ = al.align_pooled(empty, w.pairs[:0], k=w.k, X=w.X)
+        assert res.shape == (0,)
+    dev = "cuda:0"
+    z = torch.zeros((0, 4), dtype=torch.int32, device=dev)
+    xd.seed_kmer_freq_device(torch.from_numpy(w.seq).to(dev), torch.from_numpy(w.offsets).to(dev), z, 17, 1, 5,
+                             freq=torch.zeros(0, dtype=torch.int32, device=dev))
+    xd.adaptive_filter_device(torch.from_numpy(w.offsets).to(dev), z, torch.zeros((0, 5), dtype=torch.int32, device=dev),
+                              torch.zeros(0, dtype=torch.uint8, device=dev), 0.5, 1.0)
