@@ -62,6 +62,15 @@ CHILD = textwrap.dedent("""
         run(w, 300, kernel=kernel); n += 1
     w = W.config("cfg1")
     run(w, w.X); n += 1
+    # unrelated continuations at X = 500 (packed path) outgrow S = 1024: the packed S = 2048 level
+    # (pk_wide_kernel) and the 32-bit S = 4096 level read the pool through the checker too
+    w = W.random_pairs_workload(seed=661, n_pairs=12, len_lo=6000, len_hi=8000, k=11, X=500, related=0.0)
+    with xd.Aligner() as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=500)
+        assert al.stats()["cta_items"] > 0
+    ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs, w.k, w.M, w.mu, w.g, 500)
+    assert all(np.array_equal(res[f], ref[f]) for f in F) and np.array_equal(cells, rc)
+    n += 1
     print("checked ok", n)
 """)
 
@@ -70,7 +79,7 @@ def test_checked_build_every_path(checked_lib):
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True, timeout=900,
                        env=child_env(checked_lib))
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
-    assert "checked ok 21" in r.stdout
+    assert "checked ok 22" in r.stdout
 
 
 def test_checked_build_traps_out_of_bounds_reads(checked_lib):
