@@ -198,7 +198,7 @@ int dev_open(DevCtx& D, int dev) {
   D.occ_cta = std::max(1, D.occ_cta);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta1k, xk::band_cta_kernel<128, 8>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_cta2k, xk::band_cta_kernel<128, 16>, 128, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkw, xk::pk_wide_kernel, 64, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkw, xk::pk_wide_kernel<32>, 64, 0));
   D.occ_pkw = std::max(1, D.occ_pkw);
   if (const char* e = getenv("XDROP_WIDE_PK")) D.wide_pk = atoi(e);
   D.occ_cta2k = std::max(1, D.occ_cta2k);
@@ -474,7 +474,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // CTA levels: S = 2048 (4 warps x 32 lanes x 16 cells; twice the resident extensions of the
       // 8-warp block) checkpointing its overflows for S = 4096 (8 warps x 32 x 16)
       if (pk && D.wide_pk)        // packed S = 2048: one extension per 2-warp block (xdrop_pkwide.cuh)
-        xk::pk_wide_kernel<<<D.sms * D.occ_pkw, 64, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
+        xk::pk_wide_kernel<32><<<D.sms * D.occ_pkw, 64, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
       else
         xk::band_cta_kernel<128, 16><<<D.sms * D.occ_cta2k, 128, 0, s>>>(P, e4, ctr + C_HEAD4, e5, 2);
       xk::band_cta_kernel<256, 16><<<D.sms * D.occ_cta, 256, 0, s>>>(P, e5, ctr + C_HEAD5, eg, 2);

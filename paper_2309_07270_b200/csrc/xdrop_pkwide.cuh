@@ -15,7 +15,7 @@
 #pragma once
 
 namespace pkw {
-constexpr int G = 64, C = 32, NP = C / 2, S = G * C;
+constexpr int G = 64;           // lanes of the group (two warps); C cells per lane is a template parameter
 }
 
 struct PkWideShared {
@@ -39,9 +39,11 @@ __device__ __forceinline__ void pkw_min2(int& a, int& b, PkWideShared& sm) {
 }
 
 // group state from a checkpoint record of a narrower window (pk_resume_init for the 2-warp group)
-__device__ __forceinline__ void pkw_resume_init(Band16<pkw::C>& B, int gl, int& d, const int* rec, const Problem& P,
+template <int C>
+__device__ __forceinline__ void pkw_resume_init(Band16<C>& B, int gl, int& d, const int* rec, const Problem& P,
                                                 PkWideShared& sm) {
-  using namespace pkw;
+  using pkw::G;
+  constexpr int NP = C / 2, S = G * C;
   pk_geom<C>(B, P, rec[0]);
   d = rec[1];
   const int s_src = rec[14];
@@ -84,16 +86,17 @@ __device__ __forceinline__ void pkw_resume_init(Band16<pkw::C>& B, int gl, int& 
 }
 
 // one anti-diagonal d of parity PAR for the 2-warp group (pk_diag with G = 64)
-template <int PAR>
-__device__ __forceinline__ void pkw_diag(Band16<pkw::C>& B, int gl, int d, uint32_t by, uint32_t byr,
-                                         const Problem& P, const uint32_t (&chc)[2], PkWideShared& sm) {
-  using namespace pkw;
+template <int C, int PAR>
+__device__ __forceinline__ void pkw_diag(Band16<C>& B, int gl, int d, uint32_t by, uint32_t byr,
+                                         const Problem& P, const uint32_t (&chc)[C > 16 ? 2 : 1], PkWideShared& sm) {
+  using pkw::G;
+  constexpr int NP = C / 2;
   const int w = gl >> 5, lane = gl & 31;
   // the other warp's boundary value of anti-diagonal d-1 (DEAD2 at the group's own edges)
   uint32_t xs = pk::DEAD2;
   if (PAR == 1 && w == 0) xs = sm.edge[0][1];            // warp 1 lane 0's even pair 0
   if (PAR == 0 && w == 1) xs = sm.edge[1][0];            // warp 0 lane 31's odd pair NP-1
-  uint32_t ch[2];
+  uint32_t ch[C > 16 ? 2 : 1];
   uint32_t kk;
   if constexpr (PAR == 0) kk = pk_cells<C, 0, (XDROP_PK_FMA != 0), true>(B.E, B.O, B, G, gl, by, P, ch, xs);
   else kk = pk_cells<C, 1, (XDROP_PK_FMA != 0), true>(B.O, B.E, B, G, gl, by, P, ch, xs);
@@ -103,8 +106,8 @@ __device__ __forceinline__ void pkw_diag(Band16<pkw::C>& B, int gl, int d, uint3
   const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
   const int kl = ((int)kk2) >> 16;
   const uint32_t dl = pk_dead<C>(ch, chc);
-  const unsigned lb = ~(dl | byr);
-  const int tmin_l = __clz(lb) + C * gl;
+  const unsigned lb = ~(dl | byr) & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  const int tmin_l = (__clz(lb) - (32 - C)) + C * gl;
   const int tmax_l = (C - __ffs(lb)) + C * gl;
   // group key: value, then the lowest lane, then the lowest local cell (reading Q8: smallest i)
   int K = (int)((uint32_t)(kl >> 5) << 11) | ((63 - gl) << 5) | (kl & 31);
@@ -143,8 +146,9 @@ __device__ __forceinline__ void pkw_diag(Band16<pkw::C>& B, int gl, int d, uint3
 }
 
 // shift both parity arrays by one cell across the group (pk_shift1 with the warp boundary in smem)
-__device__ __forceinline__ void pkw_shift1(Band16<pkw::C>& B, int gl, int dir, PkWideShared& sm) {
-  using namespace pkw;
+template <int C>
+__device__ __forceinline__ void pkw_shift1(Band16<C>& B, int gl, int dir, PkWideShared& sm) {
+  constexpr int NP = C / 2;
   const int w = gl >> 5, lane = gl & 31;
   if (dir > 0) {                                          // cell t <- t + 1: lane takes the next lane's first
     if (lane == 0) { sm.sh[w][0] = B.E[0]; sm.sh[w][1] = B.O[0]; }
@@ -175,9 +179,10 @@ __device__ __forceinline__ void pkw_shift1(Band16<pkw::C>& B, int gl, int dir, P
 }
 
 // checkpoint for the next (S = 4096, 32-bit thread-block) level in the record format of pk_save
-__device__ __forceinline__ void pkw_save(const Band16<pkw::C>& B, int gl, int d, const Esc& e, const Problem& P,
+template <int C>
+__device__ __forceinline__ void pkw_save(const Band16<C>& B, int gl, int d, const Esc& e, const Problem& P,
                                          PkWideShared& sm) {
-  using namespace pkw;
+  constexpr int NP = C / 2, S = pkw::G * C;
   if (gl == 0) sm.q = atomicAdd(e.pool_tail, 1);
   __syncthreads();
   const int slot = sm.q;
@@ -213,9 +218,11 @@ __device__ __forceinline__ void pkw_save(const Band16<pkw::C>& B, int gl, int d,
 #ifndef XDROP_PKW_MINBLOCKS
 #define XDROP_PKW_MINBLOCKS 6
 #endif
+template <int C>
 __global__ void __launch_bounds__(64, XDROP_PKW_MINBLOCKS)
 pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
-  using namespace pkw;
+  using pkw::G;
+  constexpr int NP = C / 2, S = G * C;
   __shared__ PkWideShared sm;
   const int gl = threadIdx.x;
   const int n = *src.q_tail;
@@ -231,10 +238,10 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
     const int* rec = src.pool + (size_t)slot * src.rec_ints;
     Band16<C> B;
     pk_keys<C>(B, G, gl, P.keym >> 8);
-    uint32_t chc[2];
+    uint32_t chc[C > 16 ? 2 : 1];
     pk_chain_consts<C>(B, chc);
     int d = 0;
-    pkw_resume_init(B, gl, d, rec, P, sm);
+    pkw_resume_init<C>(B, gl, d, rec, P, sm);
     int rem = 16;
     pk_reload<C>(B, gl, rem, P);
     // the boundary values the first anti-diagonal (odd, d + 1) needs: warp 1 lane 0's even pair 0
@@ -248,8 +255,8 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
         pk_beyond<C>(B, gl, d + 1, 1, by1, byr1);
         pk_beyond<C>(B, gl, d2, 0, by2, byr2);
       }
-      pkw_diag<1>(B, gl, d + 1, by1, byr1, P, chc, sm);
-      pkw_diag<0>(B, gl, d2, by2, byr2, P, chc, sm);
+      pkw_diag<C, 1>(B, gl, d + 1, by1, byr1, P, chc, sm);
+      pkw_diag<C, 0>(B, gl, d2, by2, byr2, P, chc, sm);
       d = d2;
       // ---- block end (pk_block_end for the group)
       if (--rem == 0) {
@@ -278,11 +285,11 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
       if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
       else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
       if (ovf) {
-        pkw_save(B, gl, d, esc, P, sm);
+        pkw_save<C>(B, gl, d, esc, P, sm);
         break;
       }
       if (dir != 0) {
-        pkw_shift1(B, gl, dir, sm);
+        pkw_shift1<C>(B, gl, dir, sm);
         pk_rekey<NP>(B.E, pk_key_base(G, C, gl)); pk_rekey<NP>(B.O, pk_key_base(G, C, gl));
         B.K0 += 2 * dir; B.ia0 += dir; B.jb0 -= dir;
         pk_set_dneed<C>(B, S);
