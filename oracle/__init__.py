@@ -75,6 +75,12 @@ def _load():
             lib.oracle_align_batch.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int64] + \
                 [ctypes.c_int] * 5 + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_int64)]
+            lib.oracle_extend_mode.argtypes = lib.oracle_extend.argtypes[:8] + \
+                [ctypes.c_int, ctypes.POINTER(Ext)]
+            lib.oracle_align_mode.argtypes = lib.oracle_align.argtypes[:11] + [ctypes.c_int] + \
+                lib.oracle_align.argtypes[11:]
+            lib.oracle_align_batch_mode.argtypes = lib.oracle_align_batch.argtypes[:12] + \
+                [ctypes.c_int] + lib.oracle_align_batch.argtypes[12:]
             _lib = lib
     return _lib
 
@@ -83,23 +89,24 @@ def _b(s) -> bytes:
     return s.encode() if isinstance(s, str) else bytes(s)
 
 
-def extend(a, b, M=1, mu=-1, g=-1, X=15):
-    """EXTEND(a, b) -> (best, i*, j*, cells)   (C oracle)."""
+def extend(a, b, M=1, mu=-1, g=-1, X=15, compat=False):
+    """EXTEND(a, b) -> (best, i*, j*, cells)   (C oracle).  compat=True: the SeqAn/LOGAN-style
+    mode (Q28-Q30) -> (H of the longest extension, its i, j, cells)."""
     a, b = _b(a), _b(b)
     out = Ext()
-    rc = _load().oracle_extend(a, len(a), b, len(b), M, mu, g, X, ctypes.byref(out))
+    rc = _load().oracle_extend_mode(a, len(a), b, len(b), M, mu, g, X, int(compat), ctypes.byref(out))
     if rc:
         raise RuntimeError(f"oracle_extend failed: {rc}")
     return out.best, out.istar, out.jstar, out.cells
 
 
-def align(A, B, a_pos, b_pos, k, M=1, mu=-1, g=-1, X=15):
+def align(A, B, a_pos, b_pos, k, M=1, mu=-1, g=-1, X=15, compat=False):
     """ALIGN one pair -> dict(score, a_begin, a_end, b_begin, b_end, cells, left, right)."""
     A, B = _b(A), _b(B)
     r, c, L, R = Result(), ctypes.c_int64(), Ext(), Ext()
-    rc = _load().oracle_align(A, len(A), B, len(B), a_pos, b_pos, k, M, mu, g, X,
-                              ctypes.byref(r), ctypes.byref(c), ctypes.byref(L),
-                              ctypes.byref(R))
+    rc = _load().oracle_align_mode(A, len(A), B, len(B), a_pos, b_pos, k, M, mu, g, X, int(compat),
+                                   ctypes.byref(r), ctypes.byref(c), ctypes.byref(L),
+                                   ctypes.byref(R))
     if rc:
         raise ValueError(f"oracle_align failed: {rc}")
     return dict(score=r.score, a_begin=r.a_begin, a_end=r.a_end, b_begin=r.b_begin,
@@ -109,8 +116,9 @@ def align(A, B, a_pos, b_pos, k, M=1, mu=-1, g=-1, X=15):
 
 def align_batch(seqA: np.ndarray, offA: np.ndarray, seqB: np.ndarray, offB: np.ndarray,
                 pairs: np.ndarray, k: int, M=1, mu=-1, g=-1, X=15, nthreads=None,
-                order: np.ndarray | None = None):
+                order: np.ndarray | None = None, compat=False):
     """Batch ALIGN over read pools (uint8 ASCII + int64 offsets, pairs int32[n,4]).
+    compat=True: the SeqAn/LOGAN-style mode (Q28-Q30).
 
     Returns (results structured array RESULT_DTYPE[n], cells int64[n]).
     """
@@ -127,10 +135,10 @@ def align_batch(seqA: np.ndarray, offA: np.ndarray, seqB: np.ndarray, offB: np.n
     if nthreads is None:
         nthreads = os.cpu_count() or 1
     err = ctypes.c_int64(-1)
-    rc = _load().oracle_align_batch(
+    rc = _load().oracle_align_batch_mode(
         seqA.ctypes.data, offA.ctypes.data, seqB.ctypes.data, offB.ctypes.data,
         pairs.ctypes.data, order.ctypes.data if order is not None else None, n,
-        k, M, mu, g, X, out.ctypes.data, cells.ctypes.data, int(nthreads), ctypes.byref(err))
+        k, M, mu, g, X, int(compat), out.ctypes.data, cells.ctypes.data, int(nthreads), ctypes.byref(err))
     if rc:
         raise ValueError(f"oracle_align_batch failed rc={rc} at pair {err.value}")
     return out, cells

@@ -44,6 +44,17 @@
  *     b_begin = b_pos - L.j*, a_end = a_pos+k+R.i*, b_end = b_pos+k+R.j*,
  *     cells = L.cells + R.cells.
  *
+ *   SeqAn/LOGAN-style mode (compat = 1, DESIGN.md readings
+ *   Q28-Q30; the conventions are LOGAN's/SeqAn's, PAPER.md:85-89 names LOGAN
+ *   but prints none of them):
+ *     Q28  a pure-gap cell (i = 0 or j = 0, d >= 1) is live iff v > best - X
+ *          (strict); interior cells keep v >= best - X
+ *     Q29  the reported end is the "longest extension": the live cell of the
+ *          LAST anti-diagonal with a live cell, largest H there, ties to the
+ *          smallest i; the extension's score is H at that cell (Q30), not best
+ *     best, the thresholds, the hull, the cell count and the termination are
+ *     the same as above.
+ *
  * Storage: the values of an anti-diagonal are kept in an array indexed by i
  * (three such arrays, for d, d-1, d-2).  A slot outside the recorded hull
  * [lo,hi] of its anti-diagonal is "not live"; that is the whole bookkeeping.
@@ -97,8 +108,8 @@ static int is_live(const diag_t *D, int64_t i) {
   return D->live[i];
 }
 
-int oracle_extend(const unsigned char *a, int64_t m, const unsigned char *b, int64_t n,
-                  int M, int mu, int g, int X, oracle_ext *out) {
+int oracle_extend_mode(const unsigned char *a, int64_t m, const unsigned char *b, int64_t n,
+                       int M, int mu, int g, int X, int compat, oracle_ext *out) {
   diag_t D[3];
   for (int t = 0; t < 3; ++t) {
     D[t].H = (int32_t *)calloc((size_t)(m + 1), sizeof(int32_t));
@@ -113,6 +124,7 @@ int oracle_extend(const unsigned char *a, int64_t m, const unsigned char *b, int
   dm1->lo = 1; dm1->hi = 0; dm1->minL = 1; dm1->maxL = 0;
 
   int64_t best = 0, istar = 0, jstar = 0, cells = 1;
+  int64_t lastv = 0, lasti = 0, lastd = 0;   /* compat: max cell of the last live anti-diagonal */
   for (int64_t d = 1; d <= m + n; ++d) {
     diag_t *P1 = &D[(d - 1) % 3];   /* anti-diagonal d-1 */
     diag_t *P2 = &D[(d + 1) % 3];   /* anti-diagonal d-2  ((d-2) mod 3) */
@@ -158,6 +170,7 @@ int oracle_extend(const unsigned char *a, int64_t m, const unsigned char *b, int
         have = 1;
       }
       int lv = have && v >= thr;
+      if (compat && (i == 0 || j == 0)) lv = have && v > thr;   /* Q28: strict on the boundary */
       C->live[i] = (unsigned char)lv;
       C->H[i] = (int32_t)v;
       if (lv) {
@@ -170,31 +183,38 @@ int oracle_extend(const unsigned char *a, int64_t m, const unsigned char *b, int
     if (istar_d >= 0 && vstar > best) {
       best = vstar; istar = istar_d; jstar = d - istar_d;
     }
+    if (istar_d >= 0) { lastv = vstar; lasti = istar_d; lastd = d; }   /* Q29 */
   }
+  if (compat) { best = lastv; istar = lasti; jstar = lastd - lasti; }  /* Q29, Q30 */
   out->best = (int32_t)best; out->istar = (int32_t)istar; out->jstar = (int32_t)jstar;
   out->cells = cells;
   for (int t = 0; t < 3; ++t) { free(D[t].H); free(D[t].live); }
   return 0;
 }
 
-/* ALIGN for one pair; A, B are whole reads (ASCII). */
-int oracle_align(const unsigned char *A, int64_t lenA, const unsigned char *B, int64_t lenB,
-                 int64_t a_pos, int64_t b_pos, int k, int M, int mu, int g, int X,
-                 oracle_result *res, int64_t *cells, oracle_ext *left, oracle_ext *right) {
+int oracle_extend(const unsigned char *a, int64_t m, const unsigned char *b, int64_t n,
+                  int M, int mu, int g, int X, oracle_ext *out) {
+  return oracle_extend_mode(a, m, b, n, M, mu, g, X, 0, out);
+}
+
+/* ALIGN for one pair; A, B are whole reads (ASCII).  compat: Q28-Q30 in both extensions. */
+int oracle_align_mode(const unsigned char *A, int64_t lenA, const unsigned char *B, int64_t lenB,
+                      int64_t a_pos, int64_t b_pos, int k, int M, int mu, int g, int X, int compat,
+                      oracle_result *res, int64_t *cells, oracle_ext *left, oracle_ext *right) {
   if (a_pos < 0 || b_pos < 0 || a_pos + k > lenA || b_pos + k > lenB || k < 1) return -5;
   int64_t seed = 0;
   for (int t = 0; t < k; ++t) seed += sub_score(A[a_pos + t], B[b_pos + t], M, mu);
 
   oracle_ext R, L;
-  int rc = oracle_extend(A + a_pos + k, lenA - a_pos - k, B + b_pos + k, lenB - b_pos - k,
-                         M, mu, g, X, &R);
+  int rc = oracle_extend_mode(A + a_pos + k, lenA - a_pos - k, B + b_pos + k, lenB - b_pos - k,
+                              M, mu, g, X, compat, &R);
   if (rc) return rc;
   unsigned char *ra = (unsigned char *)malloc((size_t)a_pos + 1);
   unsigned char *rb = (unsigned char *)malloc((size_t)b_pos + 1);
   if (!ra || !rb) { free(ra); free(rb); return -2; }
   for (int64_t t = 0; t < a_pos; ++t) ra[t] = A[a_pos - 1 - t];
   for (int64_t t = 0; t < b_pos; ++t) rb[t] = B[b_pos - 1 - t];
-  rc = oracle_extend(ra, a_pos, rb, b_pos, M, mu, g, X, &L);
+  rc = oracle_extend_mode(ra, a_pos, rb, b_pos, M, mu, g, X, compat, &L);
   free(ra); free(rb);
   if (rc) return rc;
 
@@ -209,6 +229,12 @@ int oracle_align(const unsigned char *A, int64_t lenA, const unsigned char *B, i
   return 0;
 }
 
+int oracle_align(const unsigned char *A, int64_t lenA, const unsigned char *B, int64_t lenB,
+                 int64_t a_pos, int64_t b_pos, int k, int M, int mu, int g, int X,
+                 oracle_result *res, int64_t *cells, oracle_ext *left, oracle_ext *right) {
+  return oracle_align_mode(A, lenA, B, lenB, a_pos, b_pos, k, M, mu, g, X, 0, res, cells, left, right);
+}
+
 /* ---- batch over a read pool, plain thread pool ------------------------- */
 typedef struct {
   const unsigned char *seqA; const int64_t *offA;
@@ -216,7 +242,7 @@ typedef struct {
   const int32_t *pairs;      /* 4 per pair: a_id, b_id, a_pos, b_pos */
   const int64_t *order;      /* optional processing order (NULL: 0..n-1) */
   int64_t n;
-  int k, M, mu, g, X;
+  int k, M, mu, g, X, compat;
   oracle_result *out; int64_t *cells;
   volatile int64_t next;
   volatile int err; volatile int64_t err_index;
@@ -242,8 +268,8 @@ static void *worker(void *arg) {
       Bs = rcb;
     }
     int64_t c = 0;
-    int rc = oracle_align(A, lenA, Bs, lenB, q[2], q[3], B->k, B->M, B->mu, B->g, B->X,
-                          &B->out[p], &c, NULL, NULL);
+    int rc = oracle_align_mode(A, lenA, Bs, lenB, q[2], q[3], B->k, B->M, B->mu, B->g, B->X,
+                               B->compat, &B->out[p], &c, NULL, NULL);
     free(rcb);
     if (B->cells) B->cells[p] = c;
     if (rc) {
@@ -256,15 +282,15 @@ static void *worker(void *arg) {
 }
 
 /* Returns 0, or the first error code; *err_index receives the smallest failing pair. */
-int oracle_align_batch(const unsigned char *seqA, const int64_t *offA,
-                       const unsigned char *seqB, const int64_t *offB,
-                       const int32_t *pairs, const int64_t *order, int64_t n,
-                       int k, int M, int mu, int g, int X,
-                       oracle_result *out, int64_t *cells, int nthreads, int64_t *err_index) {
+int oracle_align_batch_mode(const unsigned char *seqA, const int64_t *offA,
+                            const unsigned char *seqB, const int64_t *offB,
+                            const int32_t *pairs, const int64_t *order, int64_t n,
+                            int k, int M, int mu, int g, int X, int compat,
+                            oracle_result *out, int64_t *cells, int nthreads, int64_t *err_index) {
   batch_t B;
   memset(&B, 0, sizeof(B));
   B.seqA = seqA; B.offA = offA; B.seqB = seqB; B.offB = offB; B.pairs = pairs;
-  B.order = order; B.n = n; B.k = k; B.M = M; B.mu = mu; B.g = g; B.X = X;
+  B.order = order; B.n = n; B.k = k; B.M = M; B.mu = mu; B.g = g; B.X = X; B.compat = compat;
   B.out = out; B.cells = cells; B.next = 0; B.err = 0; B.err_index = -1;
   pthread_mutex_init(&B.mu_lock, NULL);
   if (nthreads < 1) nthreads = 1;
@@ -275,4 +301,13 @@ int oracle_align_batch(const unsigned char *seqA, const int64_t *offA,
   pthread_mutex_destroy(&B.mu_lock);
   if (err_index) *err_index = B.err_index;
   return B.err;
+}
+
+int oracle_align_batch(const unsigned char *seqA, const int64_t *offA,
+                       const unsigned char *seqB, const int64_t *offB,
+                       const int32_t *pairs, const int64_t *order, int64_t n,
+                       int k, int M, int mu, int g, int X,
+                       oracle_result *out, int64_t *cells, int nthreads, int64_t *err_index) {
+  return oracle_align_batch_mode(seqA, offA, seqB, offB, pairs, order, n, k, M, mu, g, X, 0,
+                                 out, cells, nthreads, err_index);
 }

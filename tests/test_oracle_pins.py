@@ -405,3 +405,109 @@ def test_seed_kmer_freq_invariants():
     f0, _ = F.seed_kmer_freq(seq, off, np.array([[0, 0, 0, 0]], dtype=np.int32), k, 0, 99)
     f1, _ = F.seed_kmer_freq(seq2, off2, np.array([[0, 0, 0, 0], [30, 0, 0, 0]], dtype=np.int32), k, 0, 99)
     assert f1[0] == f1[1] == f0[0] + 1
+
+
+# ------------------------------------------ SeqAn/LOGAN-style mode (f3, Q28-Q30)
+def compat_impls():
+    return [("c", lambda *a: oracle.extend(*a, compat=True)),
+            ("py", lambda *a: ref.extend(*a, compat=True))]
+
+
+@pytest.mark.parametrize("name,fn", compat_impls())
+def test_compat_hand_traces(name, fn):
+    rows = []
+    with open(os.path.join(GOLDEN, "extend_compat_hand.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                lhs, rhs = line.split("|")
+                a, b, M, mu, g, X = lhs.split()
+                rows.append(("" if a == "-" else a, "" if b == "-" else b, int(M), int(mu), int(g), int(X),
+                             tuple(int(t) for t in rhs.split())))
+    assert len(rows) >= 6
+    for a, b, M, mu, g, X, want in rows:
+        assert fn(a, b, M, mu, g, X) == want, (a, b, X)
+
+
+@pytest.mark.parametrize("name,fn", compat_impls())
+def test_compat_unpruned_is_global_alignment(name, fn):
+    """With X above the no-pruning bound (strictly, so the Q28 edge rule never bites) every cell
+    lives, the last anti-diagonal is m+n, and the longest extension is the corner: (H(m,n), m, n)
+    with H(m,n) the GLOBAL alignment score -- by brute-force path enumeration on tiny inputs."""
+    pool = list(strings("AC", 3)) + list(strings(ALPH, 2))
+    for (M, mu, g) in [(1, -1, -1), (2, -3, -2)]:
+        for a in pool:
+            for b in pool:
+                X = no_prune_bound(len(a), len(b), M, mu, g) + 1
+                glob = enumerate_best(a, b, M, mu, g)[(len(a), len(b))]
+                assert fn(a, b, M, mu, g, X) == (glob, len(a), len(b), (len(a) + 1) * (len(b) + 1)), (a, b)
+
+
+def nw_global(a, b, M, mu, g):
+    """Textbook Needleman-Wunsch global score (row by row, whole table)."""
+    prev = [j * g for j in range(len(b) + 1)]
+    for i in range(1, len(a) + 1):
+        cur = [i * g] + [0] * len(b)
+        for j in range(1, len(b) + 1):
+            cur[j] = max(prev[j - 1] + (M if a[i - 1] == b[j - 1] else mu), prev[j] + g, cur[j - 1] + g)
+        prev = cur
+    return prev[-1]
+
+
+@pytest.mark.parametrize("name,fn", compat_impls())
+def test_compat_unpruned_random_nw(name, fn):
+    rng = random.Random(29)
+    for _ in range(60):
+        a = "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 20)))
+        b = mutate(rng, a, 0.2) if rng.random() < 0.6 else "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 20)))
+        for (M, mu, g) in [(1, -1, -1), (5, -4, -3)]:
+            X = no_prune_bound(len(a), len(b), M, mu, g) + 1
+            assert fn(a, b, M, mu, g, X) == (nw_global(a, b, M, mu, g), len(a), len(b),
+                                             (len(a) + 1) * (len(b) + 1)), (a, b)
+
+
+@pytest.mark.parametrize("name,fn", compat_impls())
+def test_compat_closed_forms(name, fn):
+    rng = random.Random(31)
+    # identical strings: the diagonal reaches the corner for every X >= 0
+    for L in [0, 1, 7, 31]:
+        a = "".join(rng.choice(ALPH) for _ in range(L))
+        for X in [0, 1, 15]:
+            assert fn(a, a, 2, -3, -2, X)[:3] == (2 * L, L, L)
+    # all mismatches, unit scoring, X >= 1: best stays 0, the boundary lives for j <= X-1 only (Q28),
+    # the interior square [1..X]^2 lives (H = -max(i,j) >= -X), so the last live anti-diagonal is 2X
+    # with the single cell (X,X), H = -X (Q29/Q30); computed cells: the live (X+1)^2 - 2, the two dead
+    # boundary cells (0,X), (X,0), row X+1 (j = 1..X+1) and column X+1 (i = 1..X): (X+2)^2 - 2.
+    for X in [1, 2, 5, 15]:
+        for extra in [0, 1, 7]:
+            m, n = X + 1 + extra, X + 1 + (extra * 2) % 5
+            assert fn("A" * m, "C" * n, 1, -1, -1, X) == (-X, X, X, (X + 2) ** 2 - 2)
+    # single substitution at p (unit scoring): X = 0 stops at (p,p); X >= 1 bridges it to the corner
+    for L in [4, 9, 20]:
+        a = "".join(rng.choice(ALPH) for _ in range(L))
+        for p in range(0, L - 2):
+            b = a[:p] + ALPH[(ALPH.index(a[p]) + 1) % 4] + a[p + 1:]
+            assert fn(a, b, 1, -1, -1, 0)[:3] == (p, p, p)
+            for X in [1, 2, 15]:
+                assert fn(a, b, 1, -1, -1, X)[:3] == (L - 2, L, L)
+
+
+def test_compat_twins_agree_and_align_wiring():
+    rng = random.Random(37)
+    for _ in range(300):
+        a = "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 40)))
+        b = mutate(rng, a, rng.choice([0.05, 0.15, 0.3])) if rng.random() < 0.8 else \
+            "".join(rng.choice(ALPH) for _ in range(rng.randint(0, 40)))
+        X = rng.choice([0, 1, 2, 5, 15])
+        sc = rng.choice([(1, -1, -1), (2, -3, -2), (1, -2, -1)])
+        got = oracle.extend(a, b, *sc, X, compat=True)
+        assert got == ref.extend(a, b, *sc, X, compat=True), (a, b, X, sc)
+        # the end is live on the last anti-diagonal, so it is never past the corner
+        assert 0 <= got[1] <= len(a) and 0 <= got[2] <= len(b)
+    # ALIGN composes the two compat extensions: identical reads reach both read ends
+    A = "".join(rng.choice(ALPH) for _ in range(60))
+    for pos in [0, 11, 40]:
+        r = oracle.align(A, A, pos, pos, 17, X=5, compat=True)
+        assert (r["score"], r["a_begin"], r["a_end"], r["b_begin"], r["b_end"]) == (60, 0, 60, 0, 60)
+        assert r == dict(ref.align(A, A, pos, pos, 17, X=5, compat=True),
+                         left=r["left"], right=r["right"])
