@@ -96,6 +96,15 @@ typedef struct {
  * one); results are identical either way. */
 #define XDROP_FLAG_TIERED 8        /* always the tiered kernel (small per-tier loops, short tails) */
 #define XDROP_FLAG_SHARED 16       /* always the shared kernel (one loop for every tier, no I$ thrash) */
+/* SeqAn/LOGAN-style conventions (readings Q28-Q30; LOGAN is the
+ * aligner PAPER.md:85-89 names, the conventions themselves are not in the paper): a pure-gap cell
+ * (i = 0 or j = 0) is live only if H > best - X (strict), and each extension reports its "longest
+ * extension" -- the largest-H live cell of the last anti-diagonal holding a live cell, smallest i on
+ * ties -- and H at that cell instead of the maximum (xdrop_result.score = seed + both such H;
+ * begin / end = those cells).  Thresholds, hull, `cells` and termination are the default mode's.
+ * Every extension runs in the unbounded warp-per-extension kernel (general_kernel), so this mode is
+ * an order of magnitude slower than the default one; all entry points honour it. */
+#define XDROP_FLAG_SEQAN_COMPAT 32
 
 /* A read pool in HOST memory: ASCII bases, read r = seq[offsets[r] .. offsets[r+1]). */
 typedef struct {

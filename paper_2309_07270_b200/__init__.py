@@ -26,10 +26,14 @@ class Aligner:
     """A context over one or more GPUs (``xdrop_init``)."""
 
     def __init__(self, n_devices: int = 1, devices=None, policy: str = "cells", n_ranks: int = 1,
-                 batch_size: int = 10000, subbatches: int = 1, flags: int = 0, kernel: str = "auto"):
+                 batch_size: int = 10000, subbatches: int = 1, flags: int = 0, kernel: str = "auto",
+                 seqan_compat: bool = False):
         """kernel: packed band kernel -- "auto" (per batch, from the on-device probe's escalation estimate),
-        "tiered" or "shared" (XDROP_FLAG_TIERED / XDROP_FLAG_SHARED)."""
+        "tiered" or "shared" (XDROP_FLAG_TIERED / XDROP_FLAG_SHARED).
+        seqan_compat: SeqAn/LOGAN-style conventions (XDROP_FLAG_SEQAN_COMPAT; Q28-Q30)."""
         flags |= N.KERNELS[kernel]
+        if seqan_compat:
+            flags |= N.FLAG_SEQAN_COMPAT
         opts = N.InitOpts()
         self._dev_arr = None
         if devices is not None:

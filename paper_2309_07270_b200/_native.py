@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("XDROP_LIB") or os.path.join(HERE, "libxdrop.so")   # 
 OK, EINVAL, ENOMEM, ECUDA, EALPHABET, ESEED, ELENGTH, ESTATE, ENODEV = 0, -1, -2, -3, -4, -5, -6, -7, -8
 POLICIES = {"cells": 0, "one2all": 1, "one2one": 2, "opt_one2one": 3, "mixed": 3}
 FLAG_FORCE_WIDE, FLAG_FORCE_GENERAL, FLAG_NO_SORT, FLAG_TIERED, FLAG_SHARED = 1, 2, 4, 8, 16
+FLAG_SEQAN_COMPAT = 32     # SeqAn/LOGAN-style conventions (include/xdrop.h; Q28-Q30)
 KERNELS = {"auto": 0, "tiered": FLAG_TIERED, "shared": FLAG_SHARED}   # packed band kernel (include/xdrop.h)
 MAX_READ_LEN = 1 << 18
 

@@ -72,6 +72,7 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_ZERO,                                              // always 0 (an empty queue's tail)
        C_WP, C_WT, C_WH, C_WD,                              // endgame steals of the shared kernel
        C_PROBE, C_PROBEFB,                                  // per-batch kernel probe: overflows, list tail
+       C_MAXM,                                              // longest A-side extension (unbounded path stride)
        C_N };
 constexpr int kTimelineCap = 1 << 16;
 // Per-batch choice of the packed kernel: the shared kernel when the batch's probe
@@ -238,7 +239,7 @@ int pack_pool(DevCtx& D, const char* d_seq, int64_t len, Buf& out, cudaStream_t 
   return cuda_err(cudaGetLastError());
 }
 
-struct Flags { bool force_wide, force_general, nosort, tiered, shared; };
+struct Flags { bool force_wide, force_general, nosort, tiered, shared, compat; };
 
 // The device pipeline on one GPU.  All pointers are device pointers.
 // out5 / cells may be the caller's buffers (device API) or D's workspaces.
@@ -319,7 +320,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     // a2 + a3: validate, cost estimate, length-sorted queue
     CK(cudaMemsetAsync(D.hist.p, 0, xk::NBUCKET * sizeof(int), s));
     xk::prep_kernel<<<(unsigned)((n_pairs + 255) / 256), 256, 0, s>>>(
-        P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN);
+        P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN,
+        ctr + C_MAXM);
     xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
                                        (long long)D.sms * t0b * 128, D.long_g ? D.long_alpha : 0.f,
                                        D.bad.as<unsigned long long>() + 1, ctr + C_NITEMS);
@@ -505,13 +507,16 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.long_items = hs[C_NLONG];
     D.st.stolen = hs[C_SP];
     if (n_gen > 0) {
-      const int64_t stride = XDROP_MAX_READ_LEN + 8;
+      // three anti-diagonals of m + 1 values per warp (m: the batch's longest A-side extension);
+      // all resident warps (the compat mode sends every extension here), scratch capped at 2 GiB
+      const int64_t stride = (int64_t)std::min(std::max(hs[C_MAXM], 0), XDROP_MAX_READ_LEN) + 8;
       const int warps_per_block = 4;
-      int64_t nwarps = std::min<int64_t>((int64_t)D.sms * 4, n_gen);
-      nwarps = ((nwarps + warps_per_block - 1) / warps_per_block) * warps_per_block;
+      const int64_t cap = ((int64_t)2 << 30) / (3 * stride * (int64_t)sizeof(int));
+      int64_t nwarps = std::min<int64_t>({(int64_t)D.sms * D.occ_gen * warps_per_block, (int64_t)n_gen, cap});
+      nwarps = std::max<int64_t>(warps_per_block, (nwarps / warps_per_block) * warps_per_block);
       CKR(D.scratch.ensure((size_t)nwarps * 3 * stride * sizeof(int)));
       xk::general_kernel<<<(unsigned)(nwarps / warps_per_block), 128, 0, s>>>(
-          P, gen_items, gen_count, ctr + C_HEADG, D.scratch.as<int>(), stride, 3);
+          P, gen_items, gen_count, ctr + C_HEADG, D.scratch.as<int>(), stride, 3, fl.compat ? 1 : 0);
       ++launches;
     }
   } else {
@@ -660,7 +665,9 @@ extern "C" int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st) {
 static Flags flags_of(const xdrop_ctx* ctx) {
   Flags f;
   f.force_wide = (ctx->opts.flags & XDROP_FLAG_FORCE_WIDE) != 0;
-  f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0;
+  f.compat = (ctx->opts.flags & XDROP_FLAG_SEQAN_COMPAT) != 0;
+  // the compat mode (Q28-Q30) runs every extension in the unbounded warp kernel
+  f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0 || f.compat;
   f.nosort = (ctx->opts.flags & XDROP_FLAG_NO_SORT) != 0;
   f.tiered = (ctx->opts.flags & XDROP_FLAG_TIERED) != 0;
   f.shared = (ctx->opts.flags & XDROP_FLAG_SHARED) != 0;

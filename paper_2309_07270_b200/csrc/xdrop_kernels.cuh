@@ -1459,13 +1459,16 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 // ------------------------------------------------------------ general path
 // Warp per extension, anti-diagonals indexed by i in global scratch; the hull
 // of each anti-diagonal bounds what is valid.  Unbounded band width.
+// compat != 0: the SeqAn/LOGAN-style mode (XDROP_FLAG_SEQAN_COMPAT, Q28-Q30): a pure-gap
+// cell (i = 0 or j = 0) lives only if v > best - X, and the extension reports its "longest
+// extension" -- the largest-H live cell of the last anti-diagonal with a live cell (smallest i on
+// ties) -- with H there instead of best.  Thresholds, hull, cells and termination are unchanged.
 __global__ void __launch_bounds__(128)
 general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
-               int* queue_head, int* scratch, int64_t stride, int level) {
+               int* queue_head, int* scratch, int64_t stride, int level, int compat) {
   const int lane = threadIdx.x & 31;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int* H[3];
-  for (int t = 0; t < 3; ++t) H[t] = scratch + (int64_t)warp_global * 3 * stride + t * stride;
+  int* const base = scratch + (int64_t)warp_global * 3 * stride;
   const int n_items = *n_items_ptr;
   for (;;) {
     int slot = 0;
@@ -1475,36 +1478,37 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
     const int item = items[slot];
     const Geom gm = item_geom(P, item);
     const int m = gm.m, n = gm.n;
-    int lo_[3], hi_[3], mn_[3], mx_[3];
-    // d = 0 in slot 0; d = -1 in slot 2
-    if (lane == 0) H[0][0] = BIAS;
-    lo_[0] = 0; hi_[0] = 0; mn_[0] = 0; mx_[0] = 0;
-    lo_[2] = 1; hi_[2] = 0; mn_[2] = EMIN; mx_[2] = EMAX;
-    lo_[1] = 1; hi_[1] = 0; mn_[1] = EMIN; mx_[1] = EMAX;
+    // anti-diagonals d (Hc), d-1 (H1), d-2 (H2), rotated in registers: values by i, the hull
+    // [lo, hi] computed and the live extent [mn, mx] (EMIN/EMAX: empty)
+    int *Hc = base, *H1 = base + stride, *H2 = base + 2 * stride;
+    if (lane == 0) H1[0] = BIAS;                  // d = 0: the origin; d = -1: empty
+    int lo1 = 0, hi1 = 0, mn1 = 0, mx1 = 0;
+    int lo2 = 1, hi2 = 0, mn2 = EMIN, mx2 = EMAX;
     int best = BIAS, istar = 0, jstar = 0;
+    int lastv = BIAS, lasti = 0, lastd = 0;      // compat: max cell of the last live anti-diagonal
     long long cells = 1;
+    const int cm = (int)(gm.bmask & 3ull);
     __syncwarp();
     for (int d = 1; d <= m + n; ++d) {
-      const int c = d % 3, p1 = (d + 2) % 3, p2 = (d + 1) % 3;
-      if (mn_[p1] == EMIN && mn_[p2] == EMIN) break;
-      const int lo = max(max(0, d - n), min(mn_[p1], mn_[p2] == EMIN ? EMIN : mn_[p2] + 1));
-      const int hi = min(min(m, d), max(mx_[p1], mx_[p2] == EMAX ? EMAX : mx_[p2]) + 1);
+      if (mn1 == EMIN && mn2 == EMIN) break;
+      const int lo = max(max(0, d - n), min(mn1, mn2 == EMIN ? EMIN : mn2 + 1));
+      const int hi = min(min(m, d), max(mx1, mx2 == EMAX ? EMAX : mx2) + 1);
       if (hi >= lo) cells += hi - lo + 1;
       const int thr = best - P.X;
       int kbest = NEGV, ibest = 0x7fffffff, lmn = EMIN, lmx = EMAX;
       for (int i = lo + lane; i <= hi; i += 32) {
         const int j = d - i;
         int v = NEGV;
-        if (i >= 1 && i - 1 >= lo_[p1] && i - 1 <= hi_[p1]) v = max(v, H[p1][i - 1] + P.g);
-        if (j >= 1 && i >= lo_[p1] && i <= hi_[p1]) v = max(v, H[p1][i] + P.g);
-        if (i >= 1 && j >= 1 && i - 1 >= lo_[p2] && i - 1 <= hi_[p2]) {
+        if (i >= 1 && i - 1 >= lo1 && i - 1 <= hi1) v = max(v, H1[i - 1] + P.g);
+        if (j >= 1 && i >= lo1 && i <= hi1) v = max(v, H1[i] + P.g);
+        if (i >= 1 && j >= 1 && i - 1 >= lo2 && i - 1 <= hi2) {
           const int ca = char_at(P.PA, gm.sa, gm.da, i - 1);
-          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1) ^ (int)(gm.bmask & 3ull);
-          v = max(v, H[p2][i - 1] + (ca == cb ? P.M : P.mu));
+          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1) ^ cm;
+          v = max(v, H2[i - 1] + (ca == cb ? P.M : P.mu));
         }
-        const bool live = v >= thr;
+        const bool live = (compat && (i == 0 || j == 0)) ? v > thr : v >= thr;   // Q28: strict edge
         v = live ? v : NEGV;
-        H[c][i] = v;
+        Hc[i] = v;
         if (live) {
           if (v > kbest) { kbest = v; ibest = i; }
           lmn = min(lmn, i); lmx = max(lmx, i);
@@ -1514,10 +1518,14 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
       const int gi = __reduce_min_sync(FULL, (kbest == gv) ? ibest : 0x7fffffff);
       lmn = __reduce_min_sync(FULL, lmn);
       lmx = __reduce_max_sync(FULL, lmx);
-      lo_[c] = lo; hi_[c] = hi; mn_[c] = lmn; mx_[c] = lmx;
       if (lmn != EMIN && gv > best) { best = gv; istar = gi; jstar = d - gi; }
+      if (lmn != EMIN) { lastv = gv; lasti = gi; lastd = d; }                        // Q29
+      int* const t = H2; H2 = H1; H1 = Hc; Hc = t;
+      lo2 = lo1; hi2 = hi1; mn2 = mn1; mx2 = mx1;
+      lo1 = lo; hi1 = hi; mn1 = lmn; mx1 = lmx;
       __syncwarp();
     }
+    if (compat) { best = lastv; istar = lasti; jstar = lastd - lasti; }              // Q29, Q30
     if (lane == 0) {
       ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level;
       o.cells = cells; o.pad = 0;
@@ -1598,7 +1606,7 @@ __device__ __forceinline__ bool read_ok(const int64_t* off, int64_t n, int64_t l
   return o0 >= 0 && o1 >= o0 && o1 <= len;
 }
 __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict__ hist,
-                            unsigned long long* bad_pair, int max_len) {
+                            unsigned long long* bad_pair, int max_len, int* __restrict__ max_m) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P.n_pairs) return;
   const PairDesc pd = P.pairs[p];
@@ -1612,6 +1620,8 @@ __global__ void prep_kernel(Problem P, int* __restrict__ wcost, int* __restrict_
     if (ok) {
       wl = min(pd.a_pos, pd.b_pos);
       wr = (int)min(lenA - pd.a_pos - P.k, lenB - pd.b_pos - P.k);
+      // the unbounded path indexes an anti-diagonal by i in [0, m]: its scratch stride
+      atomicMax(max_m, max(pd.a_pos, (int)(lenA - pd.a_pos - P.k)));
     }
   }
   if (!ok) atomicMin(bad_pair, (unsigned long long)p);
