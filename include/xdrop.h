@@ -222,7 +222,9 @@ int xdrop_align_multiseed(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs*
  * call (the *_ms fields: the maximum over devices and turns). */
 typedef struct {
   int64_t items;          /* extensions (2 per pair) */
-  int64_t escalated[4];   /* extensions that reached path level 1, 2, 3 (general) */
+  int64_t escalated[4];   /* extensions that reached path level 1, 2, 3 (general); with
+                             XDROP_FLAG_SEQAN_COMPAT: [0] all, [2] hulls wider than 1,024 cells
+                             (8-warp ring), [3] wider than 8,192 (global-memory kernel) */
   int64_t cells;          /* total DP cells */
   float kernel_ms;        /* CUDA-event time of the alignment kernels (all levels) */
   float total_ms;         /* CUDA-event time of the whole device pipeline */

@@ -73,6 +73,7 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_WP, C_WT, C_WH, C_WD,                              // endgame steals of the shared kernel
        C_PROBE, C_PROBEFB,                                  // per-batch kernel probe: overflows, list tail
        C_MAXM,                                              // longest A-side extension (unbounded path stride)
+       C_RINGO, C_HEADRW,                                   // compat: ring-kernel overflows, wide-ring head
        C_N };
 constexpr int kTimelineCap = 1 << 16;
 // Per-batch choice of the packed kernel: the shared kernel when the batch's probe
@@ -81,6 +82,7 @@ constexpr int kTimelineCap = 1 << 16;
 // work is then a large or long-running part of it: the shared kernel's T1/T2 pools, endgame steals
 // and in-kernel S = 1024 tier beat the tiered kernel's per-tier loops), else the tiered kernel.
 constexpr int64_t kSharedT1 = 1024;
+constexpr int kGenWideSmem = 3 * xk::kGenRingWide * (int)sizeof(int);   // general_wide_kernel's rings
 constexpr int kProbe = 4096;
 constexpr int kProbeCap = 64;
 // host mirror of the small readbacks (ints): counters at 0, bad flags at HS_BAD, level sums at HS_LVL
@@ -99,7 +101,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_ring = 1, occ_ringw = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
   int wide_pk = 1;            // S = 2048 level in the packed 2-warp kernel (XDROP_WIDE_PK=0: 32-bit CTA)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
@@ -121,7 +123,7 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw, probe;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw, probe, ringo;
   xk::PkTier tier_host[5];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
@@ -207,7 +209,11 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_SHARED_T3")) D.shared_t3 = atoi(e);
   if (const char* e = getenv("XDROP_S1024")) D.s1024 = atoi(e);
   D.occ_l0 = std::max(1, D.occ_l0); D.occ_l1 = std::max(1, D.occ_l1);
-  D.occ_l2 = std::max(1, D.occ_l2); D.occ_gen = std::max(1, D.occ_gen);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_ring, xk::general_ring_kernel, 128, 0));
+  CK(cudaFuncSetAttribute(xk::general_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenWideSmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_ringw, xk::general_wide_kernel, 256, kGenWideSmem));
+  D.occ_ringw = std::max(1, D.occ_ringw);
+  D.occ_l2 = std::max(1, D.occ_l2); D.occ_gen = std::max(1, D.occ_gen); D.occ_ring = std::max(1, D.occ_ring);
   CKR(D.h_small.ensure(HS_BYTES));
   return 0;
 }
@@ -217,7 +223,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw, &D.probe};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw, &D.probe, &D.ringo};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -368,6 +374,15 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::Esc eg{nullptr, 0, 0, ctr + C_HEADW, nullptr, nullptr, gen, ctr + C_GEN};   // always falls back
     if (fl.force_general) {
       // everything goes to the unbounded kernel below
+    } else if (fl.compat) {
+      // compat mode: the general path in shared-memory rings; hulls wider than the ring go to the
+      // unbounded kernel below (the gen list)
+      CKR(D.ringo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+      xk::general_ring_kernel<<<D.sms * D.occ_ring, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW,
+                                                                   D.ringo.as<int>(), ctr + C_RINGO, 3, 1);
+      xk::general_wide_kernel<<<D.sms * D.occ_ringw, 256, kGenWideSmem, s>>>(
+          P, D.ringo.as<int>(), ctr + C_RINGO, ctr + C_HEADRW, gen, ctr + C_GEN, 3, 1);
+      launches += 2;
     } else if (fl.force_wide) {
       xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW, e3, 1);
       ++launches;
@@ -463,6 +478,8 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     if (fl.force_general) {
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
+    } else if (fl.compat) {
+      // no band levels: the ring kernel's overflows are already in the gen list
     } else {
       // S1024 level: one warp with 32 cells per lane per extension (default), or one thread block of
       // 4 warps x 32 lanes x 8 cells (XDROP_S1024=1: slower, its barrier per anti-diagonal costs more
@@ -493,13 +510,13 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
     if (bad[1] != ~0ull) { D.err_index = (int64_t)bad[1]; return XDROP_ESEED; }
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
-    D.st.escalated[0] = fl.force_wide || fl.force_general ? n_items : hs[C_P1];
+    D.st.escalated[0] = fl.force_wide || fl.force_general || fl.compat ? n_items : hs[C_P1];
     D.st.escalated[1] = hs[C_P2];
     if (pk && !fl.force_wide && !fl.force_general && D.probe_choice == 0) {
       D.st.band_kernel = hs[C_PROBE] >= D.probe_thr ? 2 : 1;   // which kernel the probe let run
       D.st.probe_overflows = hs[C_PROBE];
     }
-    D.st.escalated[2] = hs[C_P3];
+    D.st.escalated[2] = fl.compat ? hs[C_RINGO] : hs[C_P3];   // compat: hulls wider than the warp's ring
     D.st.cta_items = hs[C_P4];
     D.st.cta4k_items = hs[C_P5];
     D.st.endgame_stolen = hs[C_WP];
@@ -665,9 +682,9 @@ extern "C" int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st) {
 static Flags flags_of(const xdrop_ctx* ctx) {
   Flags f;
   f.force_wide = (ctx->opts.flags & XDROP_FLAG_FORCE_WIDE) != 0;
+  // the compat mode (Q28-Q30) runs every extension in the general path's kernels
   f.compat = (ctx->opts.flags & XDROP_FLAG_SEQAN_COMPAT) != 0;
-  // the compat mode (Q28-Q30) runs every extension in the unbounded warp kernel
-  f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0 || f.compat;
+  f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0;
   f.nosort = (ctx->opts.flags & XDROP_FLAG_NO_SORT) != 0;
   f.tiered = (ctx->opts.flags & XDROP_FLAG_TIERED) != 0;
   f.shared = (ctx->opts.flags & XDROP_FLAG_SHARED) != 0;

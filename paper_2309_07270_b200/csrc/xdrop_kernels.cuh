@@ -1457,12 +1457,97 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 }
 
 // ------------------------------------------------------------ general path
-// Warp per extension, anti-diagonals indexed by i in global scratch; the hull
-// of each anti-diagonal bounds what is valid.  Unbounded band width.
-// compat != 0: the SeqAn/LOGAN-style mode (XDROP_FLAG_SEQAN_COMPAT, Q28-Q30): a pure-gap
-// cell (i = 0 or j = 0) lives only if v > best - X, and the extension reports its "longest
-// extension" -- the largest-H live cell of the last anti-diagonal with a live cell (smallest i on
-// ties) -- with H there instead of best.  Thresholds, hull, cells and termination are unchanged.
+// Warp per extension, one anti-diagonal's values indexed by i; the hull of each anti-diagonal
+// bounds what is valid.  compat != 0: the SeqAn/LOGAN-style mode (XDROP_FLAG_SEQAN_COMPAT,
+// DESIGN.md Q28-Q30): a pure-gap cell (i = 0 or j = 0) lives only if v > best - X, and the
+// extension reports its "longest extension" -- the largest-H live cell of the last anti-diagonal
+// with a live cell (smallest i on ties) -- with H there instead of best.  Thresholds, hull, cells
+// and termination are unchanged.
+// CAP = 0: three arrays of m + 1 values in global scratch (unbounded band width).  CAP > 0: three
+// rings of CAP values in shared memory, slot i mod CAP (exact while every hull is at most CAP
+// wide); returns false, with nothing written, as soon as a hull is wider.  NW warps work on the
+// extension (NW > 1: the whole thread block; per anti-diagonal one barrier, which also publishes
+// the per-warp reductions `red`, double-buffered by parity).
+template <int CAP, int NW>
+__device__ __forceinline__ bool gen_extend(const Problem& P, int item, int* Hc, int* H1, int* H2, int level,
+                                           int compat, int (*red)[NW][4]) {
+  constexpr int T = 32 * NW;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = NW == 1 ? lane : (int)threadIdx.x;
+  auto sync = []() { if constexpr (NW == 1) __syncwarp(); else __syncthreads(); };
+  const Geom gm = item_geom(P, item);
+  const int m = gm.m, n = gm.n;
+  auto ix = [](int i) { return CAP ? (i & (CAP - 1)) : i; };
+  // anti-diagonals d (Hc), d-1 (H1), d-2 (H2), rotated in registers: values by i, the hull
+  // [lo, hi] computed and the live extent [mn, mx] (EMIN/EMAX: empty)
+  if (t == 0) H1[0] = BIAS;                     // d = 0: the origin; d = -1: empty
+  int lo1 = 0, hi1 = 0, mn1 = 0, mx1 = 0;
+  int lo2 = 1, hi2 = 0, mn2 = EMIN, mx2 = EMAX;
+  int best = BIAS, istar = 0, jstar = 0;
+  int lastv = BIAS, lasti = 0, lastd = 0;      // compat: max cell of the last live anti-diagonal
+  long long cells = 1;
+  const int cm = (int)(gm.bmask & 3ull);
+  sync();
+  for (int d = 1; d <= m + n; ++d) {
+    if (mn1 == EMIN && mn2 == EMIN) break;
+    const int lo = max(max(0, d - n), min(mn1, mn2 == EMIN ? EMIN : mn2 + 1));
+    const int hi = min(min(m, d), max(mx1, mx2 == EMAX ? EMAX : mx2) + 1);
+    if (CAP && hi - lo + 1 > CAP) return false;   // uniform over the working threads
+    if (hi >= lo) cells += hi - lo + 1;
+    const int thr = best - P.X;
+    int kbest = NEGV, ibest = 0x7fffffff, lmn = EMIN, lmx = EMAX;
+    for (int i = lo + t; i <= hi; i += T) {
+      const int j = d - i;
+      int v = NEGV;
+      if (i >= 1 && i - 1 >= lo1 && i - 1 <= hi1) v = max(v, H1[ix(i - 1)] + P.g);
+      if (j >= 1 && i >= lo1 && i <= hi1) v = max(v, H1[ix(i)] + P.g);
+      if (i >= 1 && j >= 1 && i - 1 >= lo2 && i - 1 <= hi2) {
+        const int ca = char_at(P.PA, gm.sa, gm.da, i - 1);
+        const int cb = char_at(P.PB, gm.sb, gm.db, j - 1) ^ cm;
+        v = max(v, H2[ix(i - 1)] + (ca == cb ? P.M : P.mu));
+      }
+      const bool live = (compat && (i == 0 || j == 0)) ? v > thr : v >= thr;   // Q28: strict edge
+      v = live ? v : NEGV;
+      Hc[ix(i)] = v;
+      if (live) {
+        if (v > kbest) { kbest = v; ibest = i; }
+        lmn = min(lmn, i); lmx = max(lmx, i);
+      }
+    }
+    int gv = __reduce_max_sync(FULL, kbest);
+    int gi = __reduce_min_sync(FULL, (kbest == gv) ? ibest : 0x7fffffff);
+    lmn = __reduce_min_sync(FULL, lmn);
+    lmx = __reduce_max_sync(FULL, lmx);
+    if constexpr (NW > 1) {
+      int* r = red[d & 1][w];
+      if (lane == 0) { r[0] = gv; r[1] = gi; r[2] = lmn; r[3] = lmx; }
+      __syncthreads();
+      gv = NEGV; gi = 0x7fffffff; lmn = EMIN; lmx = EMAX;
+#pragma unroll
+      for (int u = 0; u < NW; ++u) {
+        const int* q = red[d & 1][u];
+        if (q[0] > gv || (q[0] == gv && q[1] < gi)) { gv = q[0]; gi = q[1]; }
+        lmn = min(lmn, q[2]); lmx = max(lmx, q[3]);
+      }
+    }
+    if (lmn != EMIN && gv > best) { best = gv; istar = gi; jstar = d - gi; }
+    if (lmn != EMIN) { lastv = gv; lasti = gi; lastd = d; }                        // Q29
+    int* const tmp = H2; H2 = H1; H1 = Hc; Hc = tmp;
+    lo2 = lo1; hi2 = hi1; mn2 = mn1; mx2 = mx1;
+    lo1 = lo; hi1 = hi; mn1 = lmn; mx1 = lmx;
+    if constexpr (NW == 1) __syncwarp();
+  }
+  if (compat) { best = lastv; istar = lasti; jstar = lastd - lasti; }              // Q29, Q30
+  if (t == 0) {
+    ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level;
+    o.cells = cells; o.pad = 0;
+    XDROP_CHK_ITEM(P, item);
+    P.ext[item] = o;
+  }
+  sync();
+  return true;
+}
+
+// The unbounded fallback: global scratch of 3 x stride values per warp (stride > longest m).
 __global__ void __launch_bounds__(128)
 general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
                int* queue_head, int* scratch, int64_t stride, int level, int compat) {
@@ -1475,64 +1560,53 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
     if (lane == 0) slot = atomicAdd(queue_head, 1);
     slot = __shfl_sync(FULL, slot, 0);
     if (slot >= n_items) break;
+    gen_extend<0, 1>(P, items[slot], base, base + stride, base + 2 * stride, level, compat, nullptr);
+  }
+}
+
+// The compat mode's kernels: the general path with its anti-diagonals in shared-memory rings.
+// general_ring_kernel: one warp per extension, 3 x 1,024 values per warp (48 KB per 4-warp block,
+// 4 blocks per SM); an extension whose hull outgrows its ring is queued (ovf) for
+// general_wide_kernel: one 8-warp block per extension, 3 x 8,192 values (96 KB, 2 blocks per SM),
+// which redoes it from the seed and queues the still wider ones for general_kernel.
+constexpr int kGenRing = 1024, kGenRingWide = 8192;
+__global__ void __launch_bounds__(128, 4)
+general_ring_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
+                    int* queue_head, int* ovf_items, int* ovf_count, int level, int compat) {
+  __shared__ int ring[4][3][kGenRing];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(queue_head, 1);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot >= n_items) break;
     const int item = items[slot];
-    const Geom gm = item_geom(P, item);
-    const int m = gm.m, n = gm.n;
-    // anti-diagonals d (Hc), d-1 (H1), d-2 (H2), rotated in registers: values by i, the hull
-    // [lo, hi] computed and the live extent [mn, mx] (EMIN/EMAX: empty)
-    int *Hc = base, *H1 = base + stride, *H2 = base + 2 * stride;
-    if (lane == 0) H1[0] = BIAS;                  // d = 0: the origin; d = -1: empty
-    int lo1 = 0, hi1 = 0, mn1 = 0, mx1 = 0;
-    int lo2 = 1, hi2 = 0, mn2 = EMIN, mx2 = EMAX;
-    int best = BIAS, istar = 0, jstar = 0;
-    int lastv = BIAS, lasti = 0, lastd = 0;      // compat: max cell of the last live anti-diagonal
-    long long cells = 1;
-    const int cm = (int)(gm.bmask & 3ull);
+    if (!gen_extend<kGenRing, 1>(P, item, ring[w][0], ring[w][1], ring[w][2], level, compat, nullptr) &&
+        lane == 0)
+      ovf_items[atomicAdd(ovf_count, 1)] = item;
     __syncwarp();
-    for (int d = 1; d <= m + n; ++d) {
-      if (mn1 == EMIN && mn2 == EMIN) break;
-      const int lo = max(max(0, d - n), min(mn1, mn2 == EMIN ? EMIN : mn2 + 1));
-      const int hi = min(min(m, d), max(mx1, mx2 == EMAX ? EMAX : mx2) + 1);
-      if (hi >= lo) cells += hi - lo + 1;
-      const int thr = best - P.X;
-      int kbest = NEGV, ibest = 0x7fffffff, lmn = EMIN, lmx = EMAX;
-      for (int i = lo + lane; i <= hi; i += 32) {
-        const int j = d - i;
-        int v = NEGV;
-        if (i >= 1 && i - 1 >= lo1 && i - 1 <= hi1) v = max(v, H1[i - 1] + P.g);
-        if (j >= 1 && i >= lo1 && i <= hi1) v = max(v, H1[i] + P.g);
-        if (i >= 1 && j >= 1 && i - 1 >= lo2 && i - 1 <= hi2) {
-          const int ca = char_at(P.PA, gm.sa, gm.da, i - 1);
-          const int cb = char_at(P.PB, gm.sb, gm.db, j - 1) ^ cm;
-          v = max(v, H2[i - 1] + (ca == cb ? P.M : P.mu));
-        }
-        const bool live = (compat && (i == 0 || j == 0)) ? v > thr : v >= thr;   // Q28: strict edge
-        v = live ? v : NEGV;
-        Hc[i] = v;
-        if (live) {
-          if (v > kbest) { kbest = v; ibest = i; }
-          lmn = min(lmn, i); lmx = max(lmx, i);
-        }
-      }
-      const int gv = __reduce_max_sync(FULL, kbest);
-      const int gi = __reduce_min_sync(FULL, (kbest == gv) ? ibest : 0x7fffffff);
-      lmn = __reduce_min_sync(FULL, lmn);
-      lmx = __reduce_max_sync(FULL, lmx);
-      if (lmn != EMIN && gv > best) { best = gv; istar = gi; jstar = d - gi; }
-      if (lmn != EMIN) { lastv = gv; lasti = gi; lastd = d; }                        // Q29
-      int* const t = H2; H2 = H1; H1 = Hc; Hc = t;
-      lo2 = lo1; hi2 = hi1; mn2 = mn1; mx2 = mx1;
-      lo1 = lo; hi1 = hi; mn1 = lmn; mx1 = lmx;
-      __syncwarp();
-    }
-    if (compat) { best = lastv; istar = lasti; jstar = lastd - lasti; }              // Q29, Q30
-    if (lane == 0) {
-      ExtOut o; o.best = best - BIAS; o.istar = istar; o.jstar = jstar; o.level = level;
-      o.cells = cells; o.pad = 0;
-      XDROP_CHK_ITEM(P, item);
-      P.ext[item] = o;
-    }
-    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256, 2)
+general_wide_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
+                    int* queue_head, int* ovf_items, int* ovf_count, int level, int compat) {
+  extern __shared__ int ring_w[];                 // 3 x kGenRingWide
+  __shared__ int red[2][8][4];
+  __shared__ int s_slot;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    if (threadIdx.x == 0) s_slot = atomicAdd(queue_head, 1);
+    __syncthreads();
+    const int slot = s_slot;
+    __syncthreads();
+    if (slot >= n_items) break;
+    const int item = items[slot];
+    if (!gen_extend<kGenRingWide, 8>(P, item, ring_w, ring_w + kGenRingWide, ring_w + 2 * kGenRingWide, level,
+                                     compat, red) && threadIdx.x == 0)
+      ovf_items[atomicAdd(ovf_count, 1)] = item;
+    __syncthreads();
   }
 }
 

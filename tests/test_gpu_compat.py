@@ -104,17 +104,44 @@ def test_compat_differs_from_default(xd):
 
 
 def test_compat_ecoli_and_xsweep_shapes(xd):
-    """5,000 E. coli-shaped pairs and 500 X-sweep-shaped pairs (20 kb, 20 % spurious) at X = 50."""
+    """5,000 E. coli-shaped pairs and 500 X-sweep-shaped pairs (20 kb, 20 % spurious) at X = 50 and
+    X = 100; at X = 100 some hulls outgrow the warp's shared-memory ring (1,024 cells) and are redone
+    by the 8-warp ring kernel (stats()["escalated"][2])."""
     from synth import workload as W
-    for name, scale, X in [("ecoli", 0.05, 15), ("xsweep", 0.05, 50)]:
+    for name, scale, X in [("ecoli", 0.05, 15), ("xsweep", 0.05, 50), ("xsweep", 0.05, 100)]:
         w = W.config(name, scale=scale).with_X(X)
         with xd.Aligner(seqan_compat=True) as al:
             res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
             st = al.stats()
         ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, X)
-        assert_same(res, cells, ref, rcells, f"compat {name}")
+        assert_same(res, cells, ref, rcells, f"compat {name} X={X}")
         print(f"compat {name} x{scale} X={X}: {cells.sum() / st['kernel_ms'] / 1e6:.1f} GCUPS "
-              f"({st['kernel_ms']:.1f} ms kernel)")
+              f"({st['kernel_ms']:.1f} ms kernel, ring overflows {st['escalated'][2:]})")
+        if X == 100:
+            assert st["escalated"][2] > 0
+
+
+def test_compat_unbounded_hulls(xd):
+    """Unrelated 12 kb reads seeded at their first base, X = 12,000: the right extension's hull grows
+    to the full anti-diagonal (> 8,192 cells), past both shared-memory rings, so it ends in the
+    global-memory kernel; still bit-exact."""
+    rng = np.random.default_rng(990)
+    k, L = 11, 12_000
+    reads = []
+    for _ in range(2):
+        a = rng.integers(0, 4, size=L, dtype=np.uint8)
+        b = rng.integers(0, 4, size=L - 300, dtype=np.uint8)
+        b[:k] = a[:k]
+        reads += [a, b]
+    seq = np.frombuffer(b"".join(np.frombuffer(b"ACGT", dtype=np.uint8)[r].tobytes() for r in reads), dtype=np.uint8)
+    off = np.concatenate([[0], np.cumsum([r.shape[0] for r in reads])]).astype(np.int64)
+    pairs = np.array([[0, 1, 0, 0], [2, 3, 0, 0]], dtype=np.int32)
+    with xd.Aligner(seqan_compat=True) as al:
+        res, cells = al.align(seq, off, pairs, k=k, X=L)
+        st = al.stats()
+    assert st["escalated"][3] > 0
+    ref, rcells = oracle_compat(seq, off, pairs, k, L)
+    assert_same(res, cells, ref, rcells, "compat unbounded")
 
 
 def test_compat_device_and_pooled(xd):
