@@ -13,7 +13,7 @@ import numpy as np
 from . import _native as N
 from ._native import RESULT_DTYPE, TRACE_DTYPE, XdropError  # noqa: F401
 
-__all__ = ["Aligner", "XdropError", "RESULT_DTYPE", "TRACE_DTYPE", "ring_left", "ring_right",
+__all__ = ["Aligner", "Pipeline", "XdropError", "RESULT_DTYPE", "TRACE_DTYPE", "ring_left", "ring_right",
            "sched_simulate", "alu_peaks", "pair_costs", "shard_pairs", "adaptive_filter_device",
            "seed_kmer_freq_device"]
 
@@ -231,6 +231,53 @@ class Aligner:
 
 
 PEAK_PROBES = ("VIMNMX3.S16x2", "VIMNMX3", "LOP3", "IADD3", "IMAD", "VIMNMX3.S16x2+IMAD")
+
+
+class Pipeline:
+    """Several host-API batches in flight on one GPU (a serving loop): ``n_inflight`` independent
+    contexts (``xdrop_init`` each: own device workspaces and stream), each driven by its own host
+    thread, so one batch's host-to-device upload and pack overlap another's band kernels and the
+    next batch's kernels fill the SMs a batch's tail leaves idle.  Every batch is one complete
+    ``Aligner.align`` call (its H2D, kernels and D2H); results are the same as the serial calls'.
+    ctypes releases the GIL for the duration of each C call.  DESIGN.md §9."""
+
+    def __init__(self, n_inflight: int = 3, **aligner_kwargs):
+        import queue
+        from concurrent.futures import ThreadPoolExecutor
+        self._free = queue.Queue()
+        self._als = [Aligner(**aligner_kwargs) for _ in range(max(1, int(n_inflight)))]
+        for al in self._als:
+            self._free.put(al)
+        self._pool = ThreadPoolExecutor(max_workers=len(self._als))
+
+    def _run(self, kw):
+        al = self._free.get()
+        try:
+            return al.align(**kw)
+        finally:
+            self._free.put(al)
+
+    def submit(self, seqA, offA, pairs, k: int, X: int, **kw):
+        """Queue one ``Aligner.align`` call; returns a Future of (results, cells)."""
+        return self._pool.submit(self._run, dict(seqA=seqA, offA=offA, pairs=pairs, k=k, X=X, **kw))
+
+    def map(self, batches):
+        """Align an iterable of ``align`` keyword dicts; results in order."""
+        futs = [self._pool.submit(self._run, dict(b)) for b in batches]
+        return [f.result() for f in futs]
+
+    def close(self):
+        if getattr(self, "_pool", None) is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
+            for al in self._als:
+                al.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def alu_peaks(device: int = 0) -> dict:
