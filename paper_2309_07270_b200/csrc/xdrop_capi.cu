@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -74,6 +75,7 @@ enum { C_NITEMS = 0, C_HEAD0, C_DONE0, C_HEADL, C_NLONG,   // T0 queues
        C_PROBE, C_PROBEFB,                                  // per-batch kernel probe: overflows, list tail
        C_MAXM,                                              // longest A-side extension (unbounded path stride)
        C_RINGO, C_HEADRW,                                   // compat: ring-kernel overflows, wide-ring head
+       C_GRPO, C_HEADGRP,                                   // compat: group-kernel overflows, ring-kernel head
        C_N };
 constexpr int kTimelineCap = 1 << 16;
 // Per-batch choice of the packed kernel: the shared kernel when the batch's probe
@@ -101,7 +103,7 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_ring = 1, occ_ringw = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_ring = 1, occ_ringw = 1, occ_grp = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
   int wide_pk = 1;            // S = 2048 level in the packed 2-warp kernel (XDROP_WIDE_PK=0: 32-bit CTA)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
@@ -111,6 +113,7 @@ struct DevCtx {
                            // C. elegans within 1%)
   int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
+  double compat_grp = 0.05;  // compat mode: warp rings first when this fraction of the probe overflows (XDROP_COMPAT_GRP)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per batch (probe)
   int probe_thr = 0;         // last packed call: probe threshold (0: shared forced, 2^30: tiered forced)
@@ -123,7 +126,7 @@ struct DevCtx {
   float endgame = 0.0f;     // endgame: T0 items left < endgame x resident lanes (XDROP_ENDGAME; off: measured no gain)
   // device workspaces
   Buf asciiA, asciiB, offA, offB, packA, packB, pairs, wcost, hist, cursor, items, ovf1, ovf2, ovf3,
-      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw, probe, ringo;
+      counters, bad, ext, out5, cells, scratch, level_acc, pool1, pool2, pool3, pool4, q4, pool5, q5, genl, pools, qs, tl, smcnt, ms_pairs, ms_res, ms_best, escbuf, poolw, qw, probe, ringo, grpo;
   xk::PkTier tier_host[5];          // staging of the shared packed kernel's tier descriptors (escbuf)
   // host staging (pinned)
   HostBuf h_small, h_pairs, h_res;
@@ -155,6 +158,7 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_LONG_ALPHA")) D.long_alpha = (float)atof(e);
   if (const char* e = getenv("XDROP_STEAL_MIN")) D.steal_min = atoi(e);
   if (const char* e = getenv("XDROP_STEAL_DIV")) D.steal_div = std::max(1, atoi(e));
+  if (const char* e = getenv("XDROP_COMPAT_GRP")) D.compat_grp = atof(e);
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
@@ -210,6 +214,8 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_S1024")) D.s1024 = atoi(e);
   D.occ_l0 = std::max(1, D.occ_l0); D.occ_l1 = std::max(1, D.occ_l1);
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_ring, xk::general_ring_kernel, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_grp, xk::general_group_kernel, 128, 0));
+  D.occ_grp = std::max(1, D.occ_grp);
   CK(cudaFuncSetAttribute(xk::general_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenWideSmem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_ringw, xk::general_wide_kernel, 256, kGenWideSmem));
   D.occ_ringw = std::max(1, D.occ_ringw);
@@ -223,7 +229,7 @@ void dev_close(DevCtx& D) {
   if (D.stream) cudaStreamSynchronize(D.stream);
   Buf* bufs[] = {&D.asciiA, &D.asciiB, &D.offA, &D.offB, &D.packA, &D.packB, &D.pairs, &D.wcost, &D.hist,
                  &D.cursor, &D.items, &D.ovf1, &D.ovf2, &D.ovf3, &D.counters, &D.bad, &D.ext, &D.out5,
-                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw, &D.probe, &D.ringo};
+                 &D.cells, &D.scratch, &D.level_acc, &D.pool1, &D.pool2, &D.pool3, &D.pool4, &D.q4, &D.pool5, &D.q5, &D.genl, &D.pools, &D.qs, &D.tl, &D.smcnt, &D.ms_pairs, &D.ms_res, &D.ms_best, &D.escbuf, &D.poolw, &D.qw, &D.probe, &D.ringo, &D.grpo};
   for (Buf* b : bufs) b->release();
   D.h_small.release(); D.h_pairs.release(); D.h_res.release();
   for (auto& e : D.ev) if (e) cudaEventDestroy(e);
@@ -378,11 +384,33 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // compat mode: the general path in shared-memory rings; hulls wider than the ring go to the
       // unbounded kernel below (the gen list)
       CKR(D.ringo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
-      xk::general_ring_kernel<<<D.sms * D.occ_ring, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW,
-                                                                   D.ringo.as<int>(), ctr + C_RINGO, 3, 1);
+      CKR(D.grpo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+      // group kernel (8 lanes per extension) first, unless the batch is small (< 8 extensions per
+      // resident ring warp) or the batch's probe (the default mode's, run in the packed T0 window)
+      // finds wide hulls in >= compat_grp of its sample: then the warp-ring kernel takes it directly
+      // (measured: E. coli-shaped 106 vs 190 ms with the group kernel first; X-sweep X = 15, probe
+      // 8.8 %: 53 vs 93 ms with the ring first; C. elegans-shaped x0.05, probe 4.4 %: 410 vs 492 ms)
+      xk::GenChoice gc{ctr + C_ZERO, 1 << 30};
+      if (n_items < 8LL * D.sms * D.occ_ring * 4) {
+        gc.thr = 0;      // a small batch: every extension gets its own warp at once (shorter chains)
+      } else if (pk) {
+        const int stride = (int)std::max<int64_t>(1, n_items / kProbe);
+        const int n_probe = (int)std::min<int64_t>(kProbe, (n_items + stride - 1) / stride);
+        CKR(D.probe.ensure((size_t)kProbe * sizeof(int)));
+        xk::Esc ep{nullptr, 0, 0, ctr + C_PROBE, nullptr, nullptr, D.probe.as<int>(), ctr + C_PROBEFB};
+        xk::pk_probe_kernel<32><<<(unsigned)((n_probe + 127) / 128), 128, 0, s>>>(P, items0, ctr + C_NITEMS, n_probe,
+                                                                                  stride, kProbeCap, ep);
+        ++launches;
+        gc = xk::GenChoice{ctr + C_PROBE, std::max(1, (int)std::ceil(D.compat_grp * n_probe))};
+      }
+      xk::general_group_kernel<<<D.sms * D.occ_grp, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW,
+                                                                   D.grpo.as<int>(), ctr + C_GRPO, 3, 1, gc);
+      xk::general_ring_kernel<<<D.sms * D.occ_ring, 128, 0, s>>>(P, D.grpo.as<int>(), ctr + C_GRPO, ctr + C_HEADGRP,
+                                                                   D.ringo.as<int>(), ctr + C_RINGO, 3, 1, gc,
+                                                                   items0, ctr + C_NITEMS);
       xk::general_wide_kernel<<<D.sms * D.occ_ringw, 256, kGenWideSmem, s>>>(
           P, D.ringo.as<int>(), ctr + C_RINGO, ctr + C_HEADRW, gen, ctr + C_GEN, 3, 1);
-      launches += 2;
+      launches += 3;
     } else if (fl.force_wide) {
       xk::band_kernel<32, 8><<<D.sms * D.occ_l1, 128, 0, s>>>(P, items0, ctr + C_NITEMS, ctr + C_HEADW, e3, 1);
       ++launches;
@@ -511,8 +539,9 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     if (bad[1] != ~0ull) { D.err_index = (int64_t)bad[1]; return XDROP_ESEED; }
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
     D.st.escalated[0] = fl.force_wide || fl.force_general || fl.compat ? n_items : hs[C_P1];
-    D.st.escalated[1] = hs[C_P2];
-    if (pk && !fl.force_wide && !fl.force_general && D.probe_choice == 0) {
+    D.st.escalated[1] = fl.compat ? hs[C_GRPO] : hs[C_P2];   // compat: hulls wider than a group's ring
+    if (fl.compat) D.st.probe_overflows = hs[C_PROBE];
+    if (pk && !fl.force_wide && !fl.force_general && !fl.compat && D.probe_choice == 0) {
       D.st.band_kernel = hs[C_PROBE] >= D.probe_thr ? 2 : 1;   // which kernel the probe let run
       D.st.probe_overflows = hs[C_PROBE];
     }

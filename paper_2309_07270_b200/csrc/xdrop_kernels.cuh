@@ -1468,12 +1468,33 @@ band_cta_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
 // wide); returns false, with nothing written, as soon as a hull is wider.  NW warps work on the
 // extension (NW > 1: the whole thread block; per anti-diagonal one barrier, which also publishes
 // the per-warp reductions `red`, double-buffered by parity).
-template <int CAP, int NW>
+// NW == 1 and G < 32: G lanes of the warp per extension (group-local shuffle reductions; the groups
+// of a warp run their extensions independently).
+template <int CAP, int NW, int G = 32>
 __device__ __forceinline__ bool gen_extend(const Problem& P, int item, int* Hc, int* H1, int* H2, int level,
                                            int compat, int (*red)[NW][4]) {
-  constexpr int T = 32 * NW;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = NW == 1 ? lane : (int)threadIdx.x;
-  auto sync = []() { if constexpr (NW == 1) __syncwarp(); else __syncthreads(); };
+  static_assert(NW == 1 || G == 32, "multi-warp extensions use whole warps");
+  constexpr int T = NW == 1 ? G : 32 * NW;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = NW == 1 ? (lane & (G - 1)) : (int)threadIdx.x;
+  const unsigned gmk = gmask(G);
+  auto sync = [gmk]() { if constexpr (NW == 1) __syncwarp(gmk); else __syncthreads(); };
+  auto rmax = [gmk](int v) {
+    if constexpr (G == 32) return __reduce_max_sync(FULL, v);
+    else {
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(gmk, v, o));
+      return v;
+    }
+  };
+  auto rmin = [gmk](int v) {
+    if constexpr (G == 32) return __reduce_min_sync(FULL, v);
+    else {
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(gmk, v, o));
+      return v;
+    }
+  };
   const Geom gm = item_geom(P, item);
   const int m = gm.m, n = gm.n;
   auto ix = [](int i) { return CAP ? (i & (CAP - 1)) : i; };
@@ -1513,10 +1534,10 @@ __device__ __forceinline__ bool gen_extend(const Problem& P, int item, int* Hc, 
         lmn = min(lmn, i); lmx = max(lmx, i);
       }
     }
-    int gv = __reduce_max_sync(FULL, kbest);
-    int gi = __reduce_min_sync(FULL, (kbest == gv) ? ibest : 0x7fffffff);
-    lmn = __reduce_min_sync(FULL, lmn);
-    lmx = __reduce_max_sync(FULL, lmx);
+    int gv = rmax(kbest);
+    int gi = rmin((kbest == gv) ? ibest : 0x7fffffff);
+    lmn = rmin(lmn);
+    lmx = rmax(lmx);
     if constexpr (NW > 1) {
       int* r = red[d & 1][w];
       if (lane == 0) { r[0] = gv; r[1] = gi; r[2] = lmn; r[3] = lmx; }
@@ -1534,7 +1555,7 @@ __device__ __forceinline__ bool gen_extend(const Problem& P, int item, int* Hc, 
     int* const tmp = H2; H2 = H1; H1 = Hc; Hc = tmp;
     lo2 = lo1; hi2 = hi1; mn2 = mn1; mx2 = mx1;
     lo1 = lo; hi1 = hi; mn1 = lmn; mx1 = lmx;
-    if constexpr (NW == 1) __syncwarp();
+    if constexpr (NW == 1) __syncwarp(gmk);
   }
   if (compat) { best = lastv; istar = lasti; jstar = lastd - lasti; }              // Q29, Q30
   if (t == 0) {
@@ -1565,16 +1586,48 @@ general_kernel(Problem P, const int* __restrict__ items, const int* __restrict__
 }
 
 // The compat mode's kernels: the general path with its anti-diagonals in shared-memory rings.
+// general_group_kernel: 8 lanes per extension, 4 per warp, three 256-value rings each (48 KB per
+// 4-warp block) -- most hulls are a few dozen cells wide; wider ones are queued (ovf) for
 // general_ring_kernel: one warp per extension, 3 x 1,024 values per warp (48 KB per 4-warp block,
 // 4 blocks per SM); an extension whose hull outgrows its ring is queued (ovf) for
 // general_wide_kernel: one 8-warp block per extension, 3 x 8,192 values (96 KB, 2 blocks per SM),
 // which redoes it from the seed and queues the still wider ones for general_kernel.
-constexpr int kGenRing = 1024, kGenRingWide = 8192;
+constexpr int kGenRing = 1024, kGenRingWide = 8192, kGenGroup = 8, kGenGroupRing = 256;
+// Which compat kernel takes the batch first: the group kernel unless a probe of the batch counted
+// >= thr extensions whose band outgrows 32 cells early (wide hulls: the group shape's per-anti-
+// diagonal chain would be the launch's tail), then the warp-ring kernel takes the queue directly.
+struct GenChoice { const int* cnt; int thr; };
+__global__ void __launch_bounds__(128, 4)
+general_group_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
+                     int* queue_head, int* ovf_items, int* ovf_count, int level, int compat, GenChoice ch) {
+  if (*ch.cnt >= ch.thr) return;
+  constexpr int NG = 32 / kGenGroup;
+  __shared__ int ring[4][NG][3][kGenGroupRing];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane / kGenGroup;
+  const int n_items = *n_items_ptr;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(queue_head, NG);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= n_items) break;
+    const int slot = base + g;
+    if (slot < n_items) {                                // group-uniform
+      const int item = items[slot];
+      if (!gen_extend<kGenGroupRing, 1, kGenGroup>(P, item, ring[w][g][0], ring[w][g][1], ring[w][g][2], level,
+                                                   compat, nullptr) &&
+          (lane & (kGenGroup - 1)) == 0)
+        ovf_items[atomicAdd(ovf_count, 1)] = item;
+    }
+    __syncwarp();
+  }
+}
 __global__ void __launch_bounds__(128, 4)
 general_ring_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr,
-                    int* queue_head, int* ovf_items, int* ovf_count, int level, int compat) {
+                    int* queue_head, int* ovf_items, int* ovf_count, int level, int compat, GenChoice ch,
+                    const int* __restrict__ items0, const int* __restrict__ n_items0_ptr) {
   __shared__ int ring[4][3][kGenRing];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*ch.cnt >= ch.thr) { items = items0; n_items_ptr = n_items0_ptr; }   // the group kernel stood aside
   const int n_items = *n_items_ptr;
   for (;;) {
     int slot = 0;
