@@ -103,8 +103,8 @@ typedef struct {
  * ties -- and H at that cell instead of the maximum (xdrop_result.score = seed + both such H;
  * begin / end = those cells).  Thresholds, hull, `cells` and termination are the default mode's.
  * Every extension runs in the general path's kernels (8-lane groups, warps, 8-warp blocks with
- * shared-memory rings; global memory beyond 8,192 cells), 6-9x slower than the default mode on the
- * benchmark batches; all entry points honour it. */
+ * shared-memory rings; global memory beyond 8,192 cells), 2.5-9x slower than the default mode on
+ * the benchmark batches; all entry points honour it. */
 #define XDROP_FLAG_SEQAN_COMPAT 32
 
 /* A read pool in HOST memory: ASCII bases, read r = seq[offsets[r] .. offsets[r+1]). */

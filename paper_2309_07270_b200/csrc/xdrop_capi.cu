@@ -114,6 +114,7 @@ struct DevCtx {
   int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   double compat_grp = 0.05;  // compat mode: warp rings first when this fraction of the probe overflows (XDROP_COMPAT_GRP)
+  int compat_first = 0;      // compat mode's first kernel: 0 per batch, 1 group, 2 warp ring (XDROP_COMPAT_FIRST)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per batch (probe)
   int probe_thr = 0;         // last packed call: probe threshold (0: shared forced, 2^30: tiered forced)
@@ -159,6 +160,7 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_STEAL_MIN")) D.steal_min = atoi(e);
   if (const char* e = getenv("XDROP_STEAL_DIV")) D.steal_div = std::max(1, atoi(e));
   if (const char* e = getenv("XDROP_COMPAT_GRP")) D.compat_grp = atof(e);
+  if (const char* e = getenv("XDROP_COMPAT_FIRST")) D.compat_first = atoi(e);
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
@@ -391,7 +393,9 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       // (measured: E. coli-shaped 106 vs 190 ms with the group kernel first; X-sweep X = 15, probe
       // 8.8 %: 53 vs 93 ms with the ring first; C. elegans-shaped x0.05, probe 4.4 %: 410 vs 492 ms)
       xk::GenChoice gc{ctr + C_ZERO, 1 << 30};
-      if (n_items < 8LL * D.sms * D.occ_ring * 4) {
+      if (D.compat_first == 1) {
+        // group kernel first (forced)
+      } else if (D.compat_first == 2 || n_items < 8LL * D.sms * D.occ_ring * 4) {
         gc.thr = 0;      // a small batch: every extension gets its own warp at once (shorter chains)
       } else if (pk) {
         const int stride = (int)std::max<int64_t>(1, n_items / kProbe);
