@@ -71,10 +71,13 @@ CHILD = textwrap.dedent("""
     ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs, w.k, w.M, w.mu, w.g, 500)
     assert all(np.array_equal(res[f], ref[f]) for f in F) and np.array_equal(cells, rc)
     n += 1
-    # the compat mode's general-path kernels (warp ring, 8-warp ring at X = 500)
-    for X, w in ((15, W.random_pairs_workload(seed=662, n_pairs=60, len_lo=0, len_hi=800, k=11, X=15, rc_frac=0.3)),
-                 (500, W.random_pairs_workload(seed=663, n_pairs=4, len_lo=3000, len_hi=4000, k=11, X=500,
-                                               related=0.0))):
+    # the compat mode's general-path kernels (8-lane group first, warp ring first, 8-warp ring at X = 500)
+    import os
+    wc = W.random_pairs_workload(seed=662, n_pairs=60, len_lo=0, len_hi=800, k=11, X=15, rc_frac=0.3)
+    for first, X, w in (("1", 15, wc), ("2", 15, wc),
+                        ("0", 500, W.random_pairs_workload(seed=663, n_pairs=4, len_lo=3000, len_hi=4000, k=11,
+                                                           X=500, related=0.0))):
+        os.environ["XDROP_COMPAT_FIRST"] = first
         with xd.Aligner(seqan_compat=True) as al:
             res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
             if X == 500:
@@ -91,7 +94,7 @@ def test_checked_build_every_path(checked_lib):
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, capture_output=True, text=True, timeout=900,
                        env=child_env(checked_lib))
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
-    assert "checked ok 24" in r.stdout
+    assert "checked ok 25" in r.stdout
 
 
 def test_checked_build_traps_out_of_bounds_reads(checked_lib):
