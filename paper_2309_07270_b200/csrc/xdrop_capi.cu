@@ -115,6 +115,7 @@ struct DevCtx {
   int steal_min = 1024;     // tail stealing: min anti-diagonals left (XDROP_STEAL_MIN; 0 disables)
   double compat_grp = 0.05;  // compat mode: warp rings first when this fraction of the probe overflows (XDROP_COMPAT_GRP)
   int compat_first = 0;      // compat mode's first kernel: 0 per batch, 1 group, 2 warp ring (XDROP_COMPAT_FIRST)
+  bool compat_general = false;   // compat mode in the general path only, also when packed (XDROP_COMPAT_GENERAL)
   bool timeline = false;    // XDROP_TIMELINE: record the merged kernel's work units
   int kernel_env = 0;        // XDROP_KERNEL: 1 tiered, 2 shared, 0 per batch (probe)
   int probe_thr = 0;         // last packed call: probe threshold (0: shared forced, 2^30: tiered forced)
@@ -161,6 +162,7 @@ int dev_open(DevCtx& D, int dev) {
   if (const char* e = getenv("XDROP_STEAL_DIV")) D.steal_div = std::max(1, atoi(e));
   if (const char* e = getenv("XDROP_COMPAT_GRP")) D.compat_grp = atof(e);
   if (const char* e = getenv("XDROP_COMPAT_FIRST")) D.compat_first = atoi(e);
+  if (const char* e = getenv("XDROP_COMPAT_GENERAL")) D.compat_general = atoi(e) != 0;
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
@@ -380,9 +382,14 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::Esc e4{D.pool4.as<int>(), rec4, (int)cap4, ctr + C_P4, D.q4.as<int>(), ctr + C_Q4T, gen, ctr + C_GEN};
     xk::Esc e5{D.pool5.as<int>(), rec5, (int)cap5, ctr + C_P5, D.q5.as<int>(), ctr + C_Q5T, gen, ctr + C_GEN};
     xk::Esc eg{nullptr, 0, 0, ctr + C_HEADW, nullptr, nullptr, gen, ctr + C_GEN};   // always falls back
+    // compat mode in the packed tiers: everything up to S = 1024 as in the default
+    // mode (CP instances: the Q28 edge kill, the Q29 last-maximum), wider extensions restart in the
+    // general path's rings; 32-bit cells (X + M > 510) or XDROP_COMPAT_GENERAL=1: the general path only
+    const bool cpk = fl.compat && pk && !D.compat_general;
+    xk::Esc e4c{nullptr, 0, 0, ctr + C_P4, nullptr, nullptr, gen, ctr + C_GEN};   // compat: S > 1024 -> gen
     if (fl.force_general) {
       // everything goes to the unbounded kernel below
-    } else if (fl.compat) {
+    } else if (fl.compat && !cpk) {
       // compat mode: the general path in shared-memory rings; hulls wider than the ring go to the
       // unbounded kernel below (the gen list)
       CKR(D.ringo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
@@ -454,7 +461,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         D.tier_host[0] = xk::PkTier{es, e1, nullptr, nullptr, 0};                   // fresh (T0; src: lane steals)
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
         D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
-        D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)
+        D.tier_host[3] = xk::PkTier{e3, cpk ? e4c : e4, ctr + C_HEAD3, nullptr, 2}; // T3 pool (S = 1024)
         if (!D.shared_t3) D.tier_host[3].src.q_tail = ctr + C_ZERO;                  // T3 off: an empty queue
         D.tier_host[4] = xk::PkTier{ew, e3, ctr + C_WH, ctr + C_WD, 1};             // endgame steals
         CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 5 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
@@ -482,11 +489,15 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       mcm.probe_thr = mc.probe_thr;
       const bool run_tiered = pk && choice != 2, run_shared = pk && choice != 1;
       D.st.band_kernel = pk ? (choice == 2 ? 2 : 1) : 0;   // refined from the probe count after the call
-      if (run_tiered && D.long_g == 2)
+      if (run_tiered && cpk)
+        xk::pk_tiered_kernel<4, 8, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (run_tiered && D.long_g == 2)
         xk::pk_tiered_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (run_tiered)
         xk::pk_tiered_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      if (run_shared && D.long_g == 2)
+      if (run_shared && cpk)
+        xk::pk_merged_kernel<4, 8, true><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
+      else if (run_shared && D.long_g == 2)
         xk::pk_merged_kernel<2, 16><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
       else if (run_shared)      // long_g 4, or 1 (no long mode: n_long = 0)
         xk::pk_merged_kernel<4, 8><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
@@ -510,8 +521,12 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     if (fl.force_general) {
       gen_items = items0;
       gen_count = ctr + C_NITEMS;
-    } else if (fl.compat) {
+    } else if (fl.compat && !cpk) {
       // no band levels: the ring kernel's overflows are already in the gen list
+    } else if (cpk) {
+      // compat in the packed tiers: the S = 1024 level, whose overflows restart in the general path
+      xk::pk_resume_kernel<32, 32, true><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4c, 2);
+      ++launches;
     } else {
       // S1024 level: one warp with 32 cells per lane per extension (default), or one thread block of
       // 4 warps x 32 lanes x 8 cells (XDROP_S1024=1: slower, its barrier per anti-diagonal costs more
@@ -542,20 +557,31 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     if (bad[0] != ~0ull) { D.err_index = (int64_t)bad[0]; return XDROP_EALPHABET; }
     if (bad[1] != ~0ull) { D.err_index = (int64_t)bad[1]; return XDROP_ESEED; }
     const int n_gen = fl.force_general ? (int)n_items : hs[C_GEN];
-    D.st.escalated[0] = fl.force_wide || fl.force_general || fl.compat ? n_items : hs[C_P1];
-    D.st.escalated[1] = fl.compat ? hs[C_GRPO] : hs[C_P2];   // compat: hulls wider than a group's ring
-    if (fl.compat) D.st.probe_overflows = hs[C_PROBE];
-    if (pk && !fl.force_wide && !fl.force_general && !fl.compat && D.probe_choice == 0) {
+    const bool cgen = fl.compat && !cpk;                       // compat in the general path only
+    D.st.escalated[0] = fl.force_wide || fl.force_general || cgen ? n_items : hs[C_P1];
+    D.st.escalated[1] = cgen ? hs[C_GRPO] : hs[C_P2];         // compat: hulls wider than a group's ring
+    if (cgen) D.st.probe_overflows = hs[C_PROBE];
+    if (pk && !fl.force_wide && !fl.force_general && !cgen && D.probe_choice == 0) {
       D.st.band_kernel = hs[C_PROBE] >= D.probe_thr ? 2 : 1;   // which kernel the probe let run
       D.st.probe_overflows = hs[C_PROBE];
     }
-    D.st.escalated[2] = fl.compat ? hs[C_RINGO] : hs[C_P3];   // compat: hulls wider than the warp's ring
+    D.st.escalated[2] = cgen ? hs[C_RINGO] : hs[C_P3];        // compat: hulls wider than the warp's ring
     D.st.cta_items = hs[C_P4];
     D.st.cta4k_items = hs[C_P5];
     D.st.endgame_stolen = hs[C_WP];
     D.st.escalated[3] = n_gen;
     D.st.long_items = hs[C_NLONG];
     D.st.stolen = hs[C_SP];
+    if (n_gen > 0 && cpk) {
+      // compat in the packed tiers: the extensions wider than S = 1024 restart in the 8-warp ring
+      // kernel (8,192-cell rings), whose overflows restart in the global-memory kernel below
+      CKR(D.ringo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
+      xk::general_wide_kernel<<<D.sms * D.occ_ringw, 256, kGenWideSmem, s>>>(
+          P, gen_items, gen_count, ctr + C_HEADRW, D.ringo.as<int>(), ctr + C_RINGO, 3, 1);
+      ++launches;
+      gen_items = D.ringo.as<int>();
+      gen_count = ctr + C_RINGO;
+    }
     if (n_gen > 0) {
       // three anti-diagonals of m + 1 values per warp (m: the batch's longest A-side extension);
       // all resident warps (the compat mode sends every extension here), scratch capped at 2 GiB

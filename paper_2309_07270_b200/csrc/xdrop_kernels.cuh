@@ -407,6 +407,7 @@ struct Esc {
 };
 constexpr int HDR = 32;
 constexpr int REC_T = 17;          // header int: publication time (globaltimer >> 10, ~us) of the record
+constexpr int REC_LAST = 18;       // header ints 18-20: compat mode's last-anti-diagonal maximum (packed tiers)
 __device__ __forceinline__ int rec_stamp() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -740,7 +741,7 @@ __device__ __forceinline__ int wait_entry_w(const int* q, int h, int lane) {
 #ifndef XDROP_PKR_MINBLOCKS
 #define XDROP_PKR_MINBLOCKS 3
 #endif
-template <int G, int C>
+template <int G, int C, bool CP = false>
 __global__ void __launch_bounds__(128, XDROP_PKR_MINBLOCKS)
 pk_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   constexpr int IPW = 32 / G;
@@ -754,7 +755,7 @@ pk_resume_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
     if (base >= n) break;
     const int slot = base + grp;
     const int* rec = slot < n ? src.pool + (size_t)src.q[slot] * src.rec_ints : nullptr;
-    pk_resume<G, C>(P, rec, level, esc);
+    pk_resume<G, C, CP>(P, rec, level, esc);
   }
 }
 
@@ -981,7 +982,7 @@ band_merged_kernel(Problem P, const int* __restrict__ items, const int* __restri
 //                 per warp, refilling
 //   long T0 extensions from their seed and stolen lane-mode extensions: one GL x CL instance.  T1/T2 wait for a full batch of records
 // unless the oldest queued one has waited age_us or T0 has been fully claimed.
-template <int GL, int CL>
+template <int GL, int CL, bool CP = false>
 __global__ void __launch_bounds__(128, XDROP_PKM_MINBLOCKS)
 pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  const PkTier* tiers, Steal st) {
@@ -1043,7 +1044,7 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
     if (kind == WIDE) {
       // endgame steal of a T1/T2 extension: one per warp, 32 lanes x 8 cells (S = 256), overflow to T3
       const int slot = wait_entry_w(tiers[4].src.q, h, lane);
-      pk_resume<32, 8>(P, tiers[4].src.pool + (size_t)slot * tiers[4].src.rec_ints, 1, tiers[4].esc);
+      pk_resume<32, 8, CP>(P, tiers[4].src.pool + (size_t)slot * tiers[4].src.rec_ints, 1, tiers[4].esc);
       tl_rec(c, 7, t0);
       __threadfence();
       __syncwarp();
@@ -1056,14 +1057,14 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       pk_keys<CL>(B, GL, gl, P.keym >> 8);
       if (kind == LONG) {
         const int slot = base + g;
-        pk_init_seed<CL>(B, GL, gl, slot < n_long ? items[slot] : -1, P);
+        pk_init_seed<CL, CP>(B, GL, gl, slot < n_long ? items[slot] : -1, P);
       } else {
         int slot = -1;
         if (g < k && gl == 0) slot = wait_entry(st.es.q, h + g);
         slot = __shfl_sync(FULL, slot, lane & ~(GL - 1));
-        pk_resume_init<CL>(B, GL, gl, d, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, P);
+        pk_resume_init<CL, CP>(B, GL, gl, d, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, P);
       }
-      pk_loop<CL>(B, GL, gl, d, P, 0, tiers[0].esc, nullptr);
+      pk_loop<CL, CP>(B, GL, gl, d, P, 0, tiers[0].esc, nullptr);
       tl_rec(c, kind == LONG ? 1 : 2, t0);
       __threadfence();
       __syncwarp();
@@ -1075,7 +1076,7 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       // T0 lane mode (G = 1), T1 (G = XDROP_T1_G), T2 (G = XDROP_T2_G), T3 (G = 32, S = 1024): one
       // loop instance
       const int t = kind == FRESH ? 0 : kind == T1 ? 1 : kind == T2 ? 2 : 3;
-      pk_unit<32>(P, t == 0 ? 1 : t == 1 ? XDROP_T1_G : t == 2 ? XDROP_T2_G : 32, t, tiers, items, base, n_items,
+      pk_unit<32, CP>(P, t == 0 ? 1 : t == 1 ? XDROP_T1_G : t == 2 ? XDROP_T2_G : 32, t, tiers, items, base, n_items,
                   h, k, st);
       tl_rec(c, t == 0 ? 0 : t == 1 ? 3 : t == 2 ? 4 : 6, t0);
       if (t == 0) {
@@ -1093,7 +1094,7 @@ pk_merged_kernel(Problem P, const int* __restrict__ items, const int* __restrict
 // Short anti-diagonal latency for the escalated extensions, so they never become the launch's
 // tail; but with several hot loops on an SM it stalls on instruction fetch once escalated work
 // is a large share of the batch.  xdrop_capi.cu picks it or pk_merged_kernel per call (§7).
-template <int GL, int CL>
+template <int GL, int CL, bool CP = false>
 __global__ void __launch_bounds__(128, XDROP_PKT_MINBLOCKS)
 pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict__ n_items_ptr, MergedCtr c,
                  Esc e1, Esc e2, Esc e3, Steal st) {
@@ -1117,7 +1118,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
         const int slot = wait_entry_w(e2.q, h, lane);
-        pk_resume<32, 8>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
+        pk_resume<32, 8, CP>(P, e2.pool + (size_t)slot * e2.rec_ints, 1, e3);
         tl_rec(c, 4, t0);
         continue;
       }
@@ -1135,7 +1136,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
         slot = __shfl_sync(FULL, slot, lane & ~7);
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        pk_resume<8, 8>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
+        pk_resume<8, 8, CP>(P, slot >= 0 ? e1.pool + (size_t)slot * e1.rec_ints : nullptr, 1, e2);
         tl_rec(c, 3, t0);
         __threadfence();
         __syncwarp();
@@ -1156,7 +1157,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
         slot = __shfl_sync(FULL, slot, lane & ~(GL - 1));
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        pk_resume<GL, CL>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
+        pk_resume<GL, CL, CP>(P, slot >= 0 ? st.es.pool + (size_t)slot * st.es.rec_ints : nullptr, 0, e1);
         tl_rec(c, 2, t0);
         __threadfence();
         __syncwarp();
@@ -1173,7 +1174,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
         const int slot = base + lane / GL;
         busy();
         const unsigned long long t0 = c.tl ? gtimer() : 0;
-        pk_run<GL, CL>(P, slot < n_long ? items[slot] : -1, 0, e1);
+        pk_run<GL, CL, CP>(P, slot < n_long ? items[slot] : -1, 0, e1);
         tl_rec(c, 1, t0);
         __threadfence();
         __syncwarp();
@@ -1192,7 +1193,7 @@ pk_tiered_kernel(Problem P, const int* __restrict__ items, const int* __restrict
       busy();
       const unsigned long long t0 = c.tl ? gtimer() : 0;
       const int slot = base + lane;
-      pk_run<1, XDROP_PK_C>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
+      pk_run<1, XDROP_PK_C, CP>(P, slot < n_items ? items[slot] : -1, 0, e1, &st);
       tl_rec(c, 0, t0);
       __threadfence();
       __syncwarp();

@@ -123,6 +123,7 @@ template <int C> struct Band16 {
   int cells;                      // < 2^19 anti-diagonals x 32 cells
   int item;
   bool active;
+  int lastH, lasti, lastd;        // compat mode (Q29): H + BIAS, i and d of the last live anti-diagonal's maximum
 };
 
 // key bits of a cell: 31 - t with t the cell's index in the whole window when the window has at
@@ -303,21 +304,57 @@ __device__ __forceinline__ uint32_t pk_dead(const uint32_t (&ch)[C > 16 ? 2 : 1]
 // comparing as a mismatch, lies below the real cell it descends from, hence below best_{<d}: it can
 // neither raise the threshold nor become the argmax, and byr drops it from the live extents -- the
 // same result as masking it dead, for a few instructions per anti-diagonal near the edges only.
-template <int C, int PAR, bool REDUX = true>
+// CP (compat mode, XDROP_FLAG_SEQAN_COMPAT; Q28-Q30): (a) a pure-gap cell lives only
+// strictly above the threshold.  Its W is the constant BIAS + g dbase (H = d g), the threshold in W
+// space rises by >= |g| per anti-diagonal, so the rules differ on at most the one anti-diagonal whose
+// threshold equals that constant: there the edge cells (value bits 0) are killed and the lane's key
+// maximum and live bits are recomputed from its cells.  (b) the last live anti-diagonal's maximum
+// is kept (lastH / lasti / lastd) and reported instead of the best cell.
+template <int C, int PAR, bool REDUX = true, bool CP = false>
 __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, uint32_t by, uint32_t byr,
                                         const Problem& P, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
+  constexpr int NP = C / 2;
   uint32_t ch[C > 16 ? 2 : 1];
   uint32_t kk;
   if constexpr (PAR == 0) kk = pk_cells<C, 0>(B.E, B.O, B, G, gl, by, P, ch);
   else kk = pk_cells<C, 1>(B.O, B.E, B, G, gl, by, P, ch);
   const int thr_d = B.thrN;
+  bool fixed = false;
+  uint32_t lbfix = 0;
+  if constexpr (CP) {
+    if (__any_sync(FULL, B.active && thr_d == BIAS + P.g * B.dbase)) {
+      fixed = true;
+      uint32_t (&V)[NP] = PAR == 0 ? B.E : B.O;
+      const int kb = pk_key_base(G, C, gl);
+      const int ib = (d + B.K0 + PAR) >> 1;
+      const int e0 = -ib - C * gl, e1 = d - ib - C * gl;         // local cells of i = 0 and j = 0
+      int km = -32768;
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int tl = u + NP * h;
+          int v = h ? ((int)V[u] >> 16) : (int)(int16_t)(V[u] & 0xffffu);
+          if (B.active && (tl == e0 || tl == e1) && v >= 0 && (v >> 5) == 0) {
+            const uint32_t dead = 0xC000u | (uint32_t)(kb - tl);
+            V[u] = h ? ((V[u] & 0xffffu) | (dead << 16)) : ((V[u] & 0xffff0000u) | dead);
+            v = (int)(int16_t)dead;
+          }
+          km = max(km, v);
+          if (v >= 0) lbfix |= 1u << (C - 1 - tl);
+        }
+      }
+      kk = ((uint32_t)km << 16) | ((uint32_t)km & 0xffffu);
+    }
+  }
   // key maximum over both halves: both halves of kk2 hold it; the hi half sign-extends
   const uint32_t kk2 = __vmaxs2(kk, __byte_perm(kk, 0u, 0x1032));
   const int kl = ((int)kk2) >> 16;                        // lane key: 32 * value + 31 - (local cell)
   // no live cell: kmax is a dead key (< -16128), so vrel <= -505 and neither the threshold nor best
   // can move (thrH_d = best_{<d} - X, so gv <= best - 505); no separate liveness test is needed
   const uint32_t dl = pk_dead<C>(ch, chc);
-  const unsigned lb = ~(dl | byr) & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  unsigned lb = ~(dl | byr) & (C == 32 ? 0xffffffffu : ((1u << C) - 1u));
+  if constexpr (CP) { if (fixed) lb = lbfix & ~byr & (C == 32 ? 0xffffffffu : ((1u << C) - 1u)); }
   const int tmin_l = (__clz(lb) - (32 - C)) + C * gl;
   const int tmax_l = (C - __ffs(lb)) + C * gl;
   const int ibase = (d + B.K0 + PAR) >> 1;
@@ -368,6 +405,35 @@ __device__ __forceinline__ void pk_diag(Band16<C>& B, int G, int gl, int d, uint
   const bool up = vrel > P.X;
   B.istar = up ? ibase + tst : B.istar;
   B.dstar = up ? d : B.dstar;
+  if constexpr (CP) {
+    // the maximum over REAL cells: a cell beyond the matrix (by) cannot be best but may top an
+    // anti-diagonal, so where some lane has one the key maximum is redone without them
+    int vr = vrel, ts = tst;
+    if (__any_sync(FULL, by != 0)) {
+      const uint32_t (&V)[NP] = PAR == 0 ? B.E : B.O;
+      int kr = -32768;                                   // below any 16-bit key; packs into K below
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int tl = u + NP * h;
+          const int v = h ? ((int)V[u] >> 16) : (int)(int16_t)(V[u] & 0xffffu);
+          if (!((by >> tl) & 1u)) kr = max(kr, v);
+        }
+      }
+      if (G == 1) {
+        vr = kr >> 5; ts = 31 - (kr & 31);
+      } else if (pk_global_keys(G, C)) {
+        const int km = gmax_rt(kr, G);
+        vr = km >> 5; ts = 31 - (km & 31);
+      } else {
+        int K = (int)((uint32_t)(kr >> 5) << 10) | ((31 - gl) << 5) | (kr & 31);
+        for (int o = 1; o < G; o <<= 1) K = max(K, __shfl_xor_sync(FULL, K, o));
+        vr = K >> 10; ts = C * (31 - ((K >> 5) & 31)) + 31 - (K & 31);
+      }
+    }
+    if (mn != EMIN) { B.lastH = thr_d + vr + P.g * (d - B.dbase); B.lasti = ibase + ts; B.lastd = d; }
+  }
   // hull of anti-diagonal d (reading Q5), clamped to the matrix: lo >= 0 and hi <= d hold already
   // (live cells of d-1, d-2 are inside it), lo >= d - n and hi <= m are applied here
   const int lo = max(min(B.minL1, B.minL2 + 1), d - B.n);
@@ -464,7 +530,7 @@ __device__ __forceinline__ void pk_rekey(uint32_t (&A)[NP], int kb) {
 }
 
 // checkpoint in the 32-bit record format of band_save (S = G*C; d even: E holds d, O holds d-1)
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d, const Esc& e, const Problem& P) {
   constexpr int NP = C / 2;
   int slot = 0;
@@ -480,6 +546,7 @@ __device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d
     rec[6] = B.istar; rec[7] = B.dstar - B.istar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
     rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = G * C;
     rec[15] = B.cells; rec[16] = 0; rec[REC_T] = rec_stamp();
+    if constexpr (CP) { rec[REC_LAST] = B.lastH; rec[REC_LAST + 1] = B.lasti; rec[REC_LAST + 2] = B.lastd; }
   }
 #pragma unroll
   for (int u = 0; u < NP; ++u) {
@@ -498,7 +565,7 @@ __device__ __forceinline__ void pk_save(const Band16<C>& B, int G, int gl, int d
 }
 
 // end of a block of two anti-diagonals (as band_block_end<G, C>)
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d, int& rem, const Problem& P,
                                              int level, const Esc& esc) {
   const int S = G * C;
@@ -517,6 +584,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
   if ((e0 && e1) || d >= B.m + B.n) {
     if (gl == 0) {
       ExtOut o; o.best = pk_best(B, d, P) - BIAS; o.istar = B.istar; o.jstar = B.dstar - B.istar; o.level = level;
+      if constexpr (CP) { o.best = B.lastH - BIAS; o.istar = B.lasti; o.jstar = B.lastd - B.lasti; }   // Q29, Q30
       o.cells = B.cells; o.pad = 0;
       XDROP_CHK_ITEM(P, B.item);
       P.ext[B.item] = o;
@@ -532,7 +600,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
       const int s_lo = (qmx - 2 * S + 4) >> 1;
       const int s_hi = (qmn - 2) >> 1;
       if (s_lo > s_hi) {
-        pk_save<C>(B, G, gl, d, esc, P);
+        pk_save<C, CP>(B, G, gl, d, esc, P);
         B.active = false;
         return;
       }
@@ -552,7 +620,7 @@ __device__ __forceinline__ void pk_block_end(Band16<C>& B, int G, int gl, int d,
     if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
     else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
     if (ovf) {
-      pk_save<C>(B, G, gl, d, esc, P);
+      pk_save<C, CP>(B, G, gl, d, esc, P);
       B.active = false;
       return;
     }
@@ -597,7 +665,7 @@ __device__ __forceinline__ void pk_chain_consts(const Band16<C>& B, uint32_t (&c
 
 // two anti-diagonals (d+1, d+2) and the block end; the cells beyond the matrix are flagged (pk_beyond)
 // only when some lane's window can reach them (d + 2 > dneed), else the masks are 0
-template <int C, bool REDUX = true>
+template <int C, bool REDUX = true, bool CP = false>
 __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int& rem, const Problem& P, int level,
                                         const Esc& esc, const uint32_t (&chc)[C > 16 ? 2 : 1]) {
   const int d2 = d + 2;
@@ -606,15 +674,15 @@ __device__ __forceinline__ void pk_step(Band16<C>& B, int G, int gl, int& d, int
     pk_beyond<C>(B, gl, d + 1, 1, by1, byr1);
     pk_beyond<C>(B, gl, d2, 0, by2, byr2);
   }
-  pk_diag<C, 1, REDUX>(B, G, gl, d + 1, by1, byr1, P, chc);
-  pk_diag<C, 0, REDUX>(B, G, gl, d2, by2, byr2, P, chc);
+  pk_diag<C, 1, REDUX, CP>(B, G, gl, d + 1, by1, byr1, P, chc);
+  pk_diag<C, 0, REDUX, CP>(B, G, gl, d2, by2, byr2, P, chc);
   d = d2;
-  pk_block_end<C>(B, G, gl, d, rem, P, level, esc);
+  pk_block_end<C, CP>(B, G, gl, d, rem, P, level, esc);
 }
 
 // tail stealing check (lane mode): once enough warps idle, checkpoint this lane's extension to
 // the steal queue if it still has >= min_rem anti-diagonals ahead
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, const Steal& st, const Esc& to,
                                          const Problem& P) {
   // (the group-uniform `left` test keeps pk_save's group shuffles converged for G > 1)
@@ -625,14 +693,14 @@ __device__ __forceinline__ void pk_steal(Band16<C>& B, int G, int gl, int d, con
     const int ic = (B.minL1 == EMIN) ? B.minL2 : (B.minL1 >> 1) + (B.maxL1 >> 1);
     const int left = 2 * min(B.m - ic, B.n - (d - ic));
     if (left >= st.min_rem) {
-      pk_save<C>(B, G, gl, d, to, P);
+      pk_save<C, CP>(B, G, gl, d, to, P);
       B.active = false;
     }
   }
 }
 
 // anti-diagonal loop (from an even d; groups of a warp may sit at different d)
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, const Problem& P, int level,
                                         const Esc& esc, const Steal* st) {
   uint32_t chc[C > 16 ? 2 : 1];
@@ -643,11 +711,11 @@ __device__ __forceinline__ void pk_loop(Band16<C>& B, int G, int gl, int d, cons
     if ((++blk & 31) == 0) {
       pk_rebase<C>(B, d, P);
       if (G == 1 && st != nullptr) {
-        pk_steal<C>(B, G, gl, d, *st, st->es, P);
+        pk_steal<C, CP>(B, G, gl, d, *st, st->es, P);
         if (!__any_sync(FULL, B.active)) break;
       }
     }
-    pk_step<C>(B, G, gl, d, rem, P, level, esc, chc);
+    pk_step<C, true, CP>(B, G, gl, d, rem, P, level, esc, chc);
   }
 }
 
@@ -665,7 +733,7 @@ __device__ __forceinline__ void pk_geom(Band16<C>& B, const Problem& P, int item
 }
 
 // Group state of a fresh extension at its seed (item < 0: idle group); window S = G*C <= 32.
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int item, const Problem& P) {
   constexpr int NP = C / 2;
   const int S = G * C;
@@ -684,6 +752,7 @@ __device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int it
     }
   }
   B.istar = 0; B.dstar = 0; B.cells = 1; B.dbase = 0;
+  if constexpr (CP) { B.lastH = BIAS; B.lasti = 0; B.lastd = 0; }
   B.thrD = BIAS - P.X; B.thrD1 = B.thrD; B.thrN = BIAS - P.X - P.g;     // best = BIAS (pk_best)
   B.minL1 = 0; B.maxL1 = 0; B.minL2 = EMIN; B.maxL2 = EMAX;
   pk_set_dneed<C>(B, S);
@@ -698,15 +767,15 @@ __device__ __forceinline__ void pk_init_seed(Band16<C>& B, int G, int gl, int it
 }
 
 // Run one extension per group of G lanes from its seed (item < 0: idle group).  Warp-collective.
-template <int G, int C>
+template <int G, int C, bool CP = false>
 __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, const Esc& esc,
                                        const Steal* st = nullptr) {
   static_assert(G * C <= 32 && C % 4 == 0 && C / 2 <= 16, "packed window from a seed");
   const int gl = (threadIdx.x & 31) % G;
   Band16<C> B;
   pk_keys<C>(B, G, gl, P.keym >> 8);
-  pk_init_seed<C>(B, G, gl, item, P);
-  pk_loop<C>(B, G, gl, 0, P, level, esc, st);
+  pk_init_seed<C, CP>(B, G, gl, item, P);
+  pk_loop<C, CP>(B, G, gl, 0, P, level, esc, st);
 }
 
 // Group state from a checkpoint record (rec == nullptr: idle group) in a window of S = G*C >= the
@@ -716,7 +785,7 @@ __device__ __forceinline__ void pk_run(const Problem& P, int item, int level, co
 // thr_d <= thrW_{d+1} + g, thr_{d-1} <= thr_d + g, and live values exceed their threshold by at
 // most X + M).  The recurrence only needs differences of the references, so any such T is exact.
 // Group-local: only the lanes of this group take part (a refilling pool calls it for some groups).
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int& d, const int* rec,
                                                const Problem& P) {
   constexpr int NP = C / 2;
@@ -732,6 +801,7 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
     B.istar = rec[6]; B.dstar = rec[6] + rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
     B.maxL2 = rec[11]; B.ia0 = rec[12] - sh / 2; B.jb0 = rec[13] + sh / 2;
     B.cells = rec[15];
+    if constexpr (CP) { B.lastH = rec[REC_LAST]; B.lasti = rec[REC_LAST + 1]; B.lastd = rec[REC_LAST + 2]; }
 #pragma unroll
     for (int t = 0; t < C; ++t) {
       const int qe = 2 * (C * gl + t) - sh, qo = qe + 1;
@@ -741,6 +811,7 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
   } else {
     B.K0 = -S; B.ia0 = -S / 2; B.jb0 = S / 2 - 1; B.dbase = 0; B.thrN = 0;
     B.istar = 0; B.dstar = 0; B.cells = 0; B.minL1 = EMIN; B.maxL1 = EMAX; B.minL2 = EMIN; B.maxL2 = EMAX;
+    if constexpr (CP) { B.lastH = BIAS; B.lasti = 0; B.lastd = 0; }
 #pragma unroll
     for (int t = 0; t < C; ++t) { w_e[t] = NEGV; w_o[t] = NEGV; }
   }
@@ -771,14 +842,14 @@ __device__ __forceinline__ void pk_resume_init(Band16<C>& B, int G, int gl, int&
 }
 
 // Resume one checkpointed extension per group (rec == nullptr: idle group).  Warp-collective.
-template <int G, int C>
+template <int G, int C, bool CP = false>
 __device__ __forceinline__ void pk_resume(const Problem& P, const int* rec, int level, const Esc& esc) {
   const int gl = (threadIdx.x & 31) % G;
   Band16<C> B;
   int d = 0;
   pk_keys<C>(B, G, gl, P.keym >> 8);
-  pk_resume_init<C>(B, G, gl, d, rec, P);
-  pk_loop<C>(B, G, gl, d, P, level, esc, nullptr);
+  pk_resume_init<C, CP>(B, G, gl, d, rec, P);
+  pk_loop<C, CP>(B, G, gl, d, P, level, esc, nullptr);
 }
 
 // A tier of pk_merged_kernel's shared loop, read from device memory where used (rare paths), so
@@ -792,7 +863,7 @@ struct PkTier {
 };
 
 // take up to k claimed records (queue index h..) into the idle groups of the warp (warp-collective)
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_take(Band16<C>& B, int G, int gl, int& d, int& rem, const Esc& src, int h, int k,
                                         const Problem& P) {
   const int lane = threadIdx.x & 31;
@@ -802,7 +873,7 @@ __device__ __forceinline__ void pk_take(Band16<C>& B, int G, int gl, int& d, int
     int slot = -1;
     if (gl == 0) slot = wait_entry(src.q, h + rank);
     slot = __shfl_sync(gmask(G), slot, 0, G);
-    pk_resume_init<C>(B, G, gl, d, src.pool + (size_t)slot * src.rec_ints, P);
+    pk_resume_init<C, CP>(B, G, gl, d, src.pool + (size_t)slot * src.rec_ints, P);
     rem = 16;
     pk_reload<C>(B, gl, rem, P);
   }
@@ -818,7 +889,7 @@ __device__ __forceinline__ void pk_take(Band16<C>& B, int G, int gl, int& d, int
 //        *tiers[t].done when the unit returns (after every checkpoint it wrote is published).
 // Loop-carried state beyond the extension's is kept to a few registers (the loop runs at the
 // 168-register cap of 3 blocks per SM, where every extra live value costs instructions).
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const PkTier* tiers, const int* items,
                                         int base, int n_items, int h, int k, const Steal& st) {
   const int lane = threadIdx.x & 31, gl = lane & (G - 1);
@@ -830,11 +901,11 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
   int taken = k;                                         // pool: records claimed (lane 0)
   if (t == 0) {
     const int slot = base + lane;
-    pk_init_seed<C>(B, 1, 0, slot < n_items ? items[slot] : -1, P);
+    pk_init_seed<C, CP>(B, 1, 0, slot < n_items ? items[slot] : -1, P);
     pk_reload<C>(B, gl, rem, P);
   } else {
-    pk_resume_init<C>(B, G, gl, d, nullptr, P);
-    pk_take<C>(B, G, gl, d, rem, tiers[t].src, h, k, P);
+    pk_resume_init<C, CP>(B, G, gl, d, nullptr, P);
+    pk_take<C, CP>(B, G, gl, d, rem, tiers[t].src, h, k, P);
   }
   for (int blk = 1;; ++blk) {
     if (t != 0) {
@@ -849,7 +920,7 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
           if (kk) {
             hh = __shfl_sync(FULL, hh, 0);
             taken += kk;
-            pk_take<C>(B, G, gl, d, rem, tiers[t].src, hh, kk, P);
+            pk_take<C, CP>(B, G, gl, d, rem, tiers[t].src, hh, kk, P);
           }
         }
         if (!any && kk == 0) {
@@ -867,12 +938,12 @@ __device__ __forceinline__ void pk_unit(const Problem& P, int G, int t, const Pk
       // tail stealing: lane extensions to the 4-lane queue (tiers[0].src); endgame: a T1/T2 extension
       // with a long way to go leaves the wide C = 32 shape for the latency shape (32 lanes x 8 cells,
       // tiers[4].src) once enough warps idle.  One call site (pk_save is large)
-      if (t <= 2) pk_steal<C>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src, P);
+      if (t <= 2) pk_steal<C, CP>(B, G, gl, d, st, tiers[t == 0 ? 0 : 4].src, P);
     }
     if (!__any_sync(FULL, B.active)) {
       if (t != 0) continue;                              // report and refill (or return) above
       return;
     }
-    pk_step<C, true>(B, G, gl, d, rem, P, tiers[t].level, tiers[t].esc, chc);
+    pk_step<C, true, CP>(B, G, gl, d, rem, P, tiers[t].level, tiers[t].esc, chc);
   }
 }

@@ -71,13 +71,14 @@ CHILD = textwrap.dedent("""
     ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs, w.k, w.M, w.mu, w.g, 500)
     assert all(np.array_equal(res[f], ref[f]) for f in F) and np.array_equal(cells, rc)
     n += 1
-    # the compat mode's general-path kernels (8-lane group first, warp ring first, 8-warp ring at X = 500)
+    # the compat mode: general-path kernels (8-lane group first, warp ring first), packed tiers (X = 500)
     import os
     wc = W.random_pairs_workload(seed=662, n_pairs=60, len_lo=0, len_hi=800, k=11, X=15, rc_frac=0.3)
     for first, X, w in (("1", 15, wc), ("2", 15, wc),
                         ("0", 500, W.random_pairs_workload(seed=663, n_pairs=4, len_lo=3000, len_hi=4000, k=11,
                                                            X=500, related=0.0))):
         os.environ["XDROP_COMPAT_FIRST"] = first
+        os.environ["XDROP_COMPAT_GENERAL"] = "1" if first != "0" else "0"   # "0": the packed compat path
         with xd.Aligner(seqan_compat=True) as al:
             res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=X)
             if X == 500:

@@ -65,12 +65,16 @@ def test_compat_hand_fixtures(xd):
         assert_same(res, cells, ref, rc, f"fixture {a}/{b}")
 
 
-@pytest.mark.parametrize("first", ["1", "2"])
+@pytest.mark.parametrize("path", ["packed", "group", "ring"])
 @pytest.mark.parametrize("X", [0, 1, 5, 15, 100])
-def test_compat_random_ragged(xd, X, first, monkeypatch):
-    """XDROP_COMPAT_FIRST=1: the 8-lane group kernel takes every extension first (256-cell rings,
-    overflows to the warp ring); =2: the warp-ring kernel does."""
+def test_compat_random_ragged(xd, X, path, monkeypatch):
+    """packed: the default compat path (packed tiers with the Q28 edge kill and the Q29 last maximum,
+    S > 1024 restarting in the general path); group / ring: XDROP_COMPAT_GENERAL=1, the general path
+    only, with the 8-lane group kernel (256-cell rings) or the warp-ring kernel first."""
     from synth import workload as W
+    first = {"packed": "0", "group": "1", "ring": "2"}[path]
+    if path != "packed":
+        monkeypatch.setenv("XDROP_COMPAT_GENERAL", "1")
     monkeypatch.setenv("XDROP_COMPAT_FIRST", first)
     w = W.random_pairs_workload(seed=900 + X, n_pairs=300, len_lo=0, len_hi=1500, k=11, X=X, rc_frac=0.3)
     with xd.Aligner(seqan_compat=True) as al:
@@ -79,12 +83,14 @@ def test_compat_random_ragged(xd, X, first, monkeypatch):
     if first == "1" and X == 100:
         assert st["escalated"][1] > 0          # some hulls outgrew the group's ring
     ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, X)
-    assert_same(res, cells, ref, rcells, f"compat random X={X} first={first}")
+    assert_same(res, cells, ref, rcells, f"compat random X={X} path={path}")
 
 
+@pytest.mark.parametrize("general", ["0", "1"])
 @pytest.mark.parametrize("M,mu,g", [(2, -3, -2), (1, -2, -1), (5, -4, -3)])
-def test_compat_scoring(xd, M, mu, g, monkeypatch):
+def test_compat_scoring(xd, M, mu, g, general, monkeypatch):
     from synth import workload as W
+    monkeypatch.setenv("XDROP_COMPAT_GENERAL", general)
     monkeypatch.setenv("XDROP_COMPAT_FIRST", "1")
     w = W.random_pairs_workload(seed=950 + M, n_pairs=200, len_lo=0, len_hi=800, k=9, X=12, rc_frac=0.2)
     with xd.Aligner(seqan_compat=True) as al:
