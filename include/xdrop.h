@@ -102,9 +102,9 @@ typedef struct {
  * extension" -- the largest-H live cell of the last anti-diagonal holding a live cell, smallest i on
  * ties -- and H at that cell instead of the maximum (xdrop_result.score = seed + both such H;
  * begin / end = those cells).  Thresholds, hull, `cells` and termination are the default mode's.
- * Every extension runs in the general path's kernels (8-lane groups, warps, 8-warp blocks with
- * shared-memory rings; global memory beyond 8,192 cells), 2.5-9x slower than the default mode on
- * the benchmark batches; all entry points honour it. */
+ * Packed mode (X + M <= 510): the default mode's packed tiers in compat instances up to S = 1,024,
+ * wider extensions restart in shared-memory-ring / global-memory general-path kernels; 32-bit mode
+ * (or env XDROP_COMPAT_GENERAL=1): the general path only.  All entry points honour it. */
 #define XDROP_FLAG_SEQAN_COMPAT 32
 
 /* A read pool in HOST memory: ASCII bases, read r = seq[offsets[r] .. offsets[r+1]). */
@@ -224,9 +224,9 @@ int xdrop_align_multiseed(xdrop_ctx* ctx, const xdrop_seqs* A, const xdrop_seqs*
 typedef struct {
   int64_t items;          /* extensions (2 per pair) */
   int64_t escalated[4];   /* extensions that reached path level 1, 2, 3 (general); with
-                             XDROP_FLAG_SEQAN_COMPAT: [0] all, [1] hulls wider than 256 cells
-                             (warp ring), [2] wider than 1,024 (8-warp ring), [3] wider than
-                             8,192 (global-memory kernel) */
+                             XDROP_FLAG_SEQAN_COMPAT in the general path only: [0] all,
+                             [1] hulls wider than 256 cells (warp ring), [2] wider than 1,024
+                             (8-warp ring), [3] wider than 8,192 (global-memory kernel) */
   int64_t cells;          /* total DP cells */
   float kernel_ms;        /* CUDA-event time of the alignment kernels (all levels) */
   float total_ms;         /* CUDA-event time of the whole device pipeline */
