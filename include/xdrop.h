@@ -102,7 +102,7 @@ typedef struct {
  * extension" -- the largest-H live cell of the last anti-diagonal holding a live cell, smallest i on
  * ties -- and H at that cell instead of the maximum (xdrop_result.score = seed + both such H;
  * begin / end = those cells).  Thresholds, hull, `cells` and termination are the default mode's.
- * Packed mode (X + M <= 510): the default mode's packed tiers in compat instances up to S = 1,024,
+ * Packed mode (X + M <= 510): the default mode's packed tiers in compat instances up to S = 2,048,
  * wider extensions restart in shared-memory-ring / global-memory general-path kernels; 32-bit mode
  * (or env XDROP_COMPAT_GENERAL=1): the general path only.  All entry points honour it. */
 #define XDROP_FLAG_SEQAN_COMPAT 32

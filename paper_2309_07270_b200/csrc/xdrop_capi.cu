@@ -382,11 +382,11 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     xk::Esc e4{D.pool4.as<int>(), rec4, (int)cap4, ctr + C_P4, D.q4.as<int>(), ctr + C_Q4T, gen, ctr + C_GEN};
     xk::Esc e5{D.pool5.as<int>(), rec5, (int)cap5, ctr + C_P5, D.q5.as<int>(), ctr + C_Q5T, gen, ctr + C_GEN};
     xk::Esc eg{nullptr, 0, 0, ctr + C_HEADW, nullptr, nullptr, gen, ctr + C_GEN};   // always falls back
-    // compat mode in the packed tiers: everything up to S = 1024 as in the default
+    // compat mode in the packed tiers: everything up to S = 2048 as in the default
     // mode (CP instances: the Q28 edge kill, the Q29 last-maximum), wider extensions restart in the
     // general path's rings; 32-bit cells (X + M > 510) or XDROP_COMPAT_GENERAL=1: the general path only
     const bool cpk = fl.compat && pk && !D.compat_general;
-    xk::Esc e4c{nullptr, 0, 0, ctr + C_P4, nullptr, nullptr, gen, ctr + C_GEN};   // compat: S > 1024 -> gen
+    xk::Esc e5c{nullptr, 0, 0, ctr + C_P5, nullptr, nullptr, gen, ctr + C_GEN};   // compat: S > 2048 -> gen
     if (fl.force_general) {
       // everything goes to the unbounded kernel below
     } else if (fl.compat && !cpk) {
@@ -461,7 +461,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         D.tier_host[0] = xk::PkTier{es, e1, nullptr, nullptr, 0};                   // fresh (T0; src: lane steals)
         D.tier_host[1] = xk::PkTier{e1, e2, ctr + C_Q1H, ctr + C_DONE1, 1};         // T1 pool
         D.tier_host[2] = xk::PkTier{e2, e3, ctr + C_Q2H, ctr + C_DONE2, 1};         // T2 pool
-        D.tier_host[3] = xk::PkTier{e3, cpk ? e4c : e4, ctr + C_HEAD3, nullptr, 2}; // T3 pool (S = 1024)
+        D.tier_host[3] = xk::PkTier{e3, e4, ctr + C_HEAD3, nullptr, 2};             // T3 pool (S = 1024)
         if (!D.shared_t3) D.tier_host[3].src.q_tail = ctr + C_ZERO;                  // T3 off: an empty queue
         D.tier_host[4] = xk::PkTier{ew, e3, ctr + C_WH, ctr + C_WD, 1};             // endgame steals
         CK(cudaMemcpyAsync(D.escbuf.p, D.tier_host, 5 * sizeof(xk::PkTier), cudaMemcpyHostToDevice, s));
@@ -524,9 +524,11 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     } else if (fl.compat && !cpk) {
       // no band levels: the ring kernel's overflows are already in the gen list
     } else if (cpk) {
-      // compat in the packed tiers: the S = 1024 level, whose overflows restart in the general path
-      xk::pk_resume_kernel<32, 32, true><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4c, 2);
-      ++launches;
+      // compat in the packed tiers: the S = 1024 and the packed S = 2048 levels; wider extensions
+      // restart in the general path
+      xk::pk_resume_kernel<32, 32, true><<<D.sms * D.occ_pk2, 128, 0, s>>>(P, e3, ctr + C_HEAD3, e4, 2);
+      xk::pk_wide_kernel<32, true><<<D.sms * D.occ_pkw, 64, 0, s>>>(P, e4, ctr + C_HEAD4, e5c, 2);
+      launches += 2;
     } else {
       // S1024 level: one warp with 32 cells per lane per extension (default), or one thread block of
       // 4 warps x 32 lanes x 8 cells (XDROP_S1024=1: slower, its barrier per anti-diagonal costs more
@@ -573,7 +575,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
     D.st.long_items = hs[C_NLONG];
     D.st.stolen = hs[C_SP];
     if (n_gen > 0 && cpk) {
-      // compat in the packed tiers: the extensions wider than S = 1024 restart in the 8-warp ring
+      // compat in the packed tiers: the extensions wider than S = 2048 restart in the 8-warp ring
       // kernel (8,192-cell rings), whose overflows restart in the global-memory kernel below
       CKR(D.ringo.ensure((size_t)std::max<int64_t>(1, n_items) * sizeof(int)));
       xk::general_wide_kernel<<<D.sms * D.occ_ringw, 256, kGenWideSmem, s>>>(

@@ -24,6 +24,7 @@ struct PkWideShared {
   int tmp[2][2];           // block minima / shift hand-over
   uint32_t sh[2][2];       // window shift: [warp][array E/O] boundary values
   int q;                   // claimed queue index / checkpoint slot
+  int redc[2][2];          // compat mode: [parity][warp] group key over real cells
 };
 
 // minima of a, b over the block (64 threads)
@@ -39,7 +40,7 @@ __device__ __forceinline__ void pkw_min2(int& a, int& b, PkWideShared& sm) {
 }
 
 // group state from a checkpoint record of a narrower window (pk_resume_init for the 2-warp group)
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pkw_resume_init(Band16<C>& B, int gl, int& d, const int* rec, const Problem& P,
                                                 PkWideShared& sm) {
   using pkw::G;
@@ -52,6 +53,7 @@ __device__ __forceinline__ void pkw_resume_init(Band16<C>& B, int gl, int& d, co
   B.istar = rec[6]; B.dstar = rec[6] + rec[7]; B.minL1 = rec[8]; B.maxL1 = rec[9]; B.minL2 = rec[10];
   B.maxL2 = rec[11]; B.ia0 = rec[12] - shv / 2; B.jb0 = rec[13] + shv / 2;
   B.cells = rec[15];
+  if constexpr (CP) { B.lastH = rec[REC_LAST]; B.lasti = rec[REC_LAST + 1]; B.lastd = rec[REC_LAST + 2]; }
   int w_e[C], w_o[C];
 #pragma unroll
   for (int t = 0; t < C; ++t) {
@@ -86,7 +88,9 @@ __device__ __forceinline__ void pkw_resume_init(Band16<C>& B, int gl, int& d, co
 }
 
 // one anti-diagonal d of parity PAR for the 2-warp group (pk_diag with G = 64)
-template <int C, int PAR>
+// CP: the compat mode's last-anti-diagonal maximum over real cells (pk_diag's Q29 part; the Q28
+// edge rule cannot apply here: an extension reaches this level only after d >= 1,023 > X / |g| + 1)
+template <int C, int PAR, bool CP = false>
 __device__ __forceinline__ void pkw_diag(Band16<C>& B, int gl, int d, uint32_t by, uint32_t byr,
                                          const Problem& P, const uint32_t (&chc)[C > 16 ? 2 : 1], PkWideShared& sm) {
   using pkw::G;
@@ -129,6 +133,30 @@ __device__ __forceinline__ void pkw_diag(Band16<C>& B, int gl, int d, uint32_t b
   const bool up = vrel > P.X;
   B.istar = up ? ibase + tst : B.istar;
   B.dstar = up ? d : B.dstar;
+  if constexpr (CP) {
+    int vr = vrel, ts = tst;
+    if (__syncthreads_or(by != 0)) {                    // block-uniform
+      int kr = -32768;
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int tl = u + NP * h;
+          const uint32_t x = PAR == 0 ? B.E[u] : B.O[u];
+          const int v = h ? ((int)x >> 16) : (int)(int16_t)(x & 0xffffu);
+          if (!((by >> tl) & 1u)) kr = max(kr, v);
+        }
+      }
+      int Kr = (int)((uint32_t)(kr >> 5) << 11) | ((63 - gl) << 5) | (kr & 31);
+      Kr = __reduce_max_sync(FULL, Kr);
+      if (lane == 0) sm.redc[PAR][w] = Kr;
+      __syncthreads();
+      Kr = max(sm.redc[PAR][0], sm.redc[PAR][1]);
+      vr = Kr >> 11;
+      ts = C * (63 - ((Kr >> 5) & 63)) + 31 - (Kr & 31);
+    }
+    if (mn != EMIN) { B.lastH = thr_d + vr + P.g * (d - B.dbase); B.lasti = ibase + ts; B.lastd = d; }
+  }
   const int lo = max(min(B.minL1, B.minL2 + 1), d - B.n);
   const int hi = min(max(B.maxL1, B.maxL2) + 1, B.m);
   B.cells += max(0, hi - lo + 1);
@@ -179,7 +207,7 @@ __device__ __forceinline__ void pkw_shift1(Band16<C>& B, int gl, int dir, PkWide
 }
 
 // checkpoint for the next (S = 4096, 32-bit thread-block) level in the record format of pk_save
-template <int C>
+template <int C, bool CP = false>
 __device__ __forceinline__ void pkw_save(const Band16<C>& B, int gl, int d, const Esc& e, const Problem& P,
                                          PkWideShared& sm) {
   constexpr int NP = C / 2, S = pkw::G * C;
@@ -197,6 +225,7 @@ __device__ __forceinline__ void pkw_save(const Band16<C>& B, int gl, int d, cons
     rec[6] = B.istar; rec[7] = B.dstar - B.istar; rec[8] = B.minL1; rec[9] = B.maxL1; rec[10] = B.minL2;
     rec[11] = B.maxL2; rec[12] = B.ia0; rec[13] = B.jb0; rec[14] = S;
     rec[15] = B.cells; rec[16] = 0; rec[REC_T] = rec_stamp();
+    if constexpr (CP) { rec[REC_LAST] = B.lastH; rec[REC_LAST + 1] = B.lasti; rec[REC_LAST + 2] = B.lastd; }
   }
 #pragma unroll
   for (int u = 0; u < NP; ++u) {
@@ -218,7 +247,7 @@ __device__ __forceinline__ void pkw_save(const Band16<C>& B, int gl, int d, cons
 #ifndef XDROP_PKW_MINBLOCKS
 #define XDROP_PKW_MINBLOCKS 6
 #endif
-template <int C>
+template <int C, bool CP = false>
 __global__ void __launch_bounds__(64, XDROP_PKW_MINBLOCKS)
 pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
   using pkw::G;
@@ -241,7 +270,7 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
     uint32_t chc[C > 16 ? 2 : 1];
     pk_chain_consts<C>(B, chc);
     int d = 0;
-    pkw_resume_init<C>(B, gl, d, rec, P, sm);
+    pkw_resume_init<C, CP>(B, gl, d, rec, P, sm);
     int rem = 16;
     pk_reload<C>(B, gl, rem, P);
     // the boundary values the first anti-diagonal (odd, d + 1) needs: warp 1 lane 0's even pair 0
@@ -255,8 +284,8 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
         pk_beyond<C>(B, gl, d + 1, 1, by1, byr1);
         pk_beyond<C>(B, gl, d2, 0, by2, byr2);
       }
-      pkw_diag<C, 1>(B, gl, d + 1, by1, byr1, P, chc, sm);
-      pkw_diag<C, 0>(B, gl, d2, by2, byr2, P, chc, sm);
+      pkw_diag<C, 1, CP>(B, gl, d + 1, by1, byr1, P, chc, sm);
+      pkw_diag<C, 0, CP>(B, gl, d2, by2, byr2, P, chc, sm);
       d = d2;
       // ---- block end (pk_block_end for the group)
       if (--rem == 0) {
@@ -271,6 +300,7 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
       if ((e0 && e1) || d >= B.m + B.n) {
         if (gl == 0) {
           ExtOut o; o.best = pk_best(B, d, P) - BIAS; o.istar = B.istar; o.jstar = B.dstar - B.istar;
+          if constexpr (CP) { o.best = B.lastH - BIAS; o.istar = B.lasti; o.jstar = B.lastd - B.lasti; }
           o.level = level; o.cells = B.cells; o.pad = 0;
           XDROP_CHK_ITEM(P, B.item);
           P.ext[B.item] = o;
@@ -285,7 +315,7 @@ pk_wide_kernel(Problem P, Esc src, int* queue_head, Esc esc, int level) {
       if (qmx >= 2 * S - 2) { if (qmn >= 4) dir = 1; else ovf = true; }
       else if (qmn <= 1) { if (qmx <= 2 * S - 5) dir = -1; else ovf = true; }
       if (ovf) {
-        pkw_save<C>(B, gl, d, esc, P, sm);
+        pkw_save<C, CP>(B, gl, d, esc, P, sm);
         break;
       }
       if (dir != 0) {
