@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="pair-count scale (tests only)")
     ap.add_argument("--X", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-compat", action="store_true", help="skip the compat-mode (XDROP_FLAG_SEQAN_COMPAT) entry")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the bounded oracle sample")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
@@ -233,7 +234,7 @@ def ncu_traffic(args, kregex):
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "-k", f"regex:{kregex}", "--launch-skip", str(warm), "--launch-count", "1",
            "--csv", sys.executable, os.path.abspath(__file__), "--steps", "1", "--warmup", str(warm),
-           "--no-e2e", "--no-cpu", "--no-traffic", "--config", args.config, "--scale", str(args.scale)]
+           "--no-e2e", "--no-cpu", "--no-traffic", "--no-compat", "--config", args.config, "--scale", str(args.scale)]
     if args.X is not None:
         cmd += ["--X", str(args.X)]
     try:
@@ -528,6 +529,41 @@ def run_native(args, world, rank, local):
             print(f"PARITY FAILURE: {int(bad.sum())} of {idx.shape[0]} sampled pairs differ from the oracle",
                   file=sys.stderr)
 
+    # the SeqAn/LOGAN-style compat mode (XDROP_FLAG_SEQAN_COMPAT, Q28-Q30) on the same
+    # HBM-resident batch: device-timed like `value` (its own cell count), checked against the oracle's
+    # compat mode on evenly spaced pairs (informational; not the headline)
+    compat = None
+    if world == 1 and not args.no_compat:
+        with xd.Aligner(devices=[local], seqan_compat=True) as alc:
+            oc = torch.zeros_like(out_d)
+            cc = torch.zeros_like(cells_d)
+            for _ in range(2):
+                alc.align_device(seq_d, off_d, pairs_d, oc, cc, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g, stream=stream)
+            torch.cuda.synchronize(dev)
+            cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+            for a, b in cev:
+                flush.zero_()
+                a.record(stream)
+                alc.align_device(seq_d, off_d, pairs_d, oc, cc, k=w.k, X=w.X, M=w.M, mu=w.mu, g=w.g, stream=stream)
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            c_ms = min(a.elapsed_time(b) for a, b in cev)
+        c_cells = int(cc.sum().item())
+        compat = {"value": round(c_cells / (c_ms * 1e-3) / 1e9, 3), "unit": "GCUPS", "ms_per_step": round(c_ms, 3),
+                  "cells_per_step": c_cells, "steps": 3, "note": "best of 3 steps, device-resident batch"}
+        if rank == 0 and not args.no_cpu:
+            import oracle
+            idx = np.linspace(0, n_my - 1, min(n_my, 2000)).astype(np.int64)
+            ref, rc = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, my_pairs[idx], w.k, M=w.M, mu=w.mu,
+                                         g=w.g, X=w.X, compat=True)
+            o = oc.cpu().numpy()[idx]
+            c = cc.cpu().numpy()[idx]
+            bad = np.zeros(idx.shape[0], dtype=bool)
+            for i, f in enumerate(("score", "a_begin", "a_end", "b_begin", "b_end")):
+                bad |= o[:, i] != ref[f]
+            bad |= c != rc
+            compat["parity"] = {"checked": int(idx.shape[0]), "mismatches": int(bad.sum())}
+
     if rank == 0:
         line = {"metric": METRIC,
                 "value": round(gcups, 3), "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
@@ -543,7 +579,8 @@ def run_native(args, world, rank, local):
                 "e2e": e2e, "gpu_launches": int(sum(s["launches"] for s in stats) * world),
                 "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "clocks": clocks,
                 "escalated_per_step": stats[-1]["escalated"][:3],
-                "level_ms": [round(float(x), 3) for x in lvl_ms], "step_ms_all": [round(x, 3) for x in step_ms]}
+                "level_ms": [round(float(x), 3) for x in lvl_ms], "step_ms_all": [round(x, 3) for x in step_ms],
+                "compat": compat}
         emit(line, args)
     al.close()
 
