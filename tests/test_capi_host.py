@@ -28,6 +28,18 @@ def test_exports_every_declared_symbol(xd):
     assert set(N.EXPORTS) <= declared
 
 
+def test_binding_constants_match_header(xd):
+    """The binding's flag / policy values are the header's (the C ABI is the contract)."""
+    from paper_2309_07270_b200 import _native as N
+    hdr = open(os.path.join(ROOT, "include", "xdrop.h")).read()
+    flags = {k: int(v) for k, v in re.findall(r"^#define XDROP_FLAG_(\w+)\s+(\d+)", hdr, re.M)}
+    assert flags == {"FORCE_WIDE": N.FLAG_FORCE_WIDE, "FORCE_GENERAL": N.FLAG_FORCE_GENERAL,
+                     "NO_SORT": N.FLAG_NO_SORT, "TIERED": N.FLAG_TIERED, "SHARED": N.FLAG_SHARED,
+                     "SEQAN_COMPAT": N.FLAG_SEQAN_COMPAT}
+    pol = {k.lower(): int(v) for k, v in re.findall(r"XDROP_POLICY_(\w+)\s*=\s*(\d+)", hdr)}
+    assert all(N.POLICIES[k] == v for k, v in pol.items()) and len(pol) == 4
+
+
 def test_strerror_and_no_device_fails_loudly(xd):
     from paper_2309_07270_b200 import _native as N
     assert N.lib.xdrop_strerror(-4) == b"base outside {A,C,G,T}"
