@@ -209,3 +209,18 @@ def test_compat_every_pair_configs_2_4(xd, name, X):
     res, cells = _device_run(xd, w)
     ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, X)
     assert_same(res, cells, ref, rcells, f"compat every pair {name} X={X}")
+
+
+def test_compat_multiseed(xd):
+    """xdrop_align_multiseed in the compat mode: every seed row aligned with Q28-Q30 and the best
+    seed chosen on those scores (Q26 on the compat scores), against the oracle's."""
+    import oracle
+    from synth import workload as W
+    w = W.make_pool_workload("ms-compat", 92, 200_000, 150, W._normal_len(2000, 300, 800, 4000), 8.0, 300,
+                             k=15, X=15, rc_frac=0.3, seeds_per_pair=3, f_sp=0.1)
+    ref, rcells = oracle.align_batch(w.seq, w.offsets, w.seq, w.offsets, w.pairs, w.k, X=w.X, compat=True)
+    rbest = oracle.best_seed(w.pairs, ref["score"])
+    with xd.Aligner(seqan_compat=True) as al:
+        res, best, cells = al.align_multiseed(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    assert_same(res, cells, ref, rcells, "compat multiseed")
+    assert np.array_equal(best, rbest)
