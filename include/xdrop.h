@@ -87,7 +87,7 @@ typedef struct {
   int flags;            /* XDROP_FLAG_* */
 } xdrop_init_opts;
 
-#define XDROP_FLAG_FORCE_WIDE 1    /* skip the lane-per-extension path (tests) */
+#define XDROP_FLAG_FORCE_WIDE 1    /* skip the lane-per-extension path (tests; ignored with SEQAN_COMPAT) */
 #define XDROP_FLAG_FORCE_GENERAL 2 /* send every extension to the unbounded fallback (tests) */
 #define XDROP_FLAG_NO_SORT 4       /* do not length-sort the work queue (tests) */
 /* Packed-mode band kernel (X + M <= 510).  Default: chosen per batch on the device by

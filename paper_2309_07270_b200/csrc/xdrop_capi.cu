@@ -743,8 +743,9 @@ extern "C" int xdrop_last_stats(const xdrop_ctx* ctx, xdrop_stats* st) {
 static Flags flags_of(const xdrop_ctx* ctx) {
   Flags f;
   f.force_wide = (ctx->opts.flags & XDROP_FLAG_FORCE_WIDE) != 0;
-  // the compat mode (Q28-Q30) runs every extension in the general path's kernels
+  // the compat mode (Q28-Q30): the packed tiers' CP instances or the general path
   f.compat = (ctx->opts.flags & XDROP_FLAG_SEQAN_COMPAT) != 0;
+  if (f.compat) f.force_wide = false;     // the 32-bit warp level has no compat instance
   f.force_general = (ctx->opts.flags & XDROP_FLAG_FORCE_GENERAL) != 0;
   f.nosort = (ctx->opts.flags & XDROP_FLAG_NO_SORT) != 0;
   f.tiered = (ctx->opts.flags & XDROP_FLAG_TIERED) != 0;

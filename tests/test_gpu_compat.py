@@ -224,3 +224,15 @@ def test_compat_multiseed(xd):
         res, best, cells = al.align_multiseed(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
     assert_same(res, cells, ref, rcells, "compat multiseed")
     assert np.array_equal(best, rbest)
+
+
+@pytest.mark.parametrize("flags", [1, 2, 4, 8, 16])
+def test_compat_with_test_flags(xd, flags):
+    """Compat mode combined with every other XDROP_FLAG_* (FORCE_WIDE is ignored: the 32-bit warp level
+    has no compat instance; FORCE_GENERAL runs the unbounded kernel; NO_SORT, TIERED, SHARED as named)."""
+    from synth import workload as W
+    w = W.random_pairs_workload(seed=1300 + flags, n_pairs=120, len_lo=0, len_hi=1200, k=11, X=20, rc_frac=0.3)
+    with xd.Aligner(seqan_compat=True, flags=flags) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=20)
+    ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, 20)
+    assert_same(res, cells, ref, rcells, f"compat flags={flags}")
