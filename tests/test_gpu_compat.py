@@ -236,3 +236,15 @@ def test_compat_with_test_flags(xd, flags):
         res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=20)
     ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, 20)
     assert_same(res, cells, ref, rcells, f"compat flags={flags}")
+
+
+@pytest.mark.parametrize("policy,n_ranks", [("cells", 1), ("one2all", 4), ("one2one", 4), ("opt_one2one", 4)])
+def test_compat_policies_logical_devices(xd, policy, n_ranks):
+    """The compat mode under every scheduler policy on three logical devices (streams of GPU 0):
+    results identical to the oracle's compat mode."""
+    from synth import workload as W
+    w = W.config("cfg1")
+    with xd.Aligner(devices=[0, 0, 0], policy=policy, n_ranks=n_ranks, batch_size=37, seqan_compat=True) as al:
+        res, cells = al.align(w.seq, w.offsets, w.pairs, k=w.k, X=w.X)
+    ref, rcells = oracle_compat(w.seq, w.offsets, w.pairs, w.k, w.X)
+    assert_same(res, cells, ref, rcells, f"compat {policy}")
