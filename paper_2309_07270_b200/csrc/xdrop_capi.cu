@@ -103,12 +103,13 @@ struct DevCtx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_ring = 1, occ_ringw = 1, occ_grp = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
+  int occ_l0 = 1, occ_l1 = 1, occ_l2 = 1, occ_gen = 1, occ_ring = 1, occ_ringw = 1, occ_grp = 1, occ_m = 1, occ_pk = 1, occ_pkm = 1, occ_pk8 = 1, occ_pkm8 = 1, occ_pk2 = 1, occ_pkw = 1, occ_cta = 1, occ_cta1k = 1, occ_cta2k = 1;
   int shared_t3 = 1;          // shared kernel resumes S1024 records itself (XDROP_SHARED_T3=0: the CTA launch)
   int wide_pk = 1;            // S = 2048 level in the packed 2-warp kernel (XDROP_WIDE_PK=0: 32-bit CTA)
   int s1024 = 0;              // S1024 level after the band kernel: 0 warp 32x32, 1 CTA<128,8> (XDROP_S1024;
                               // measured slower: X-sweep X=50 59 -> 95 ms, the per-anti-diagonal barrier)
-  int long_g = 4;          // lanes per long extension (XDROP_LONG_G: 0 disables, 2 or 4)
+  int long_g = -1;         // lanes per long extension: -1 per call (4 below X = 32, 8 from it: DESIGN.md
+                           // §7), XDROP_LONG_G fixes it (0 disables the long mode, 2, 4 or 8)
   float long_alpha = 2.0f; // long cut (XDROP_LONG_ALPHA; 2 measured best: E. coli 12.2 -> 11.7 ms vs 1, X-sweep and
                            // C. elegans within 1%)
   int steal_div = 8;         // stealing starts once resident warps / steal_div are idle (XDROP_STEAL_DIV)
@@ -166,12 +167,16 @@ int dev_open(DevCtx& D, int dev) {
   D.timeline = getenv("XDROP_TIMELINE") != nullptr;
   if (const char* e = getenv("XDROP_ENDGAME")) D.endgame = (float)atof(e);
   if (const char* e = getenv("XDROP_PK16")) D.pk16 = atoi(e) != 0;
-  if (D.long_g != 0 && D.long_g != 2 && D.long_g != 4) D.long_g = 4;
+  if (D.long_g != -1 && D.long_g != 0 && D.long_g != 2 && D.long_g != 4 && D.long_g != 8) D.long_g = -1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk8, xk::pk_tiered_kernel<8, 4>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm8, xk::pk_merged_kernel<8, 4>, 128, 0));
+  D.occ_pk8 = std::max(1, D.occ_pk8);
+  D.occ_pkm8 = std::max(1, D.occ_pkm8);
   if (D.long_g == 2) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 2, 16>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<2, 16>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm, xk::pk_merged_kernel<2, 16>, 128, 0));
-  } else if (D.long_g == 4) {
+  } else if (D.long_g == 4 || D.long_g == 8 || D.long_g == -1) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_m, xk::band_merged_kernel<32, 4, 8>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pk, xk::pk_tiered_kernel<4, 8>, 128, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.occ_pkm, xk::pk_merged_kernel<4, 8>, 128, 0));
@@ -324,7 +329,11 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
   const bool pk = D.pk16 && p.xdrop + p.match <= 510;
   // resident blocks per SM of the tiered (or 32-bit merged) kernel and of the shared kernel, and how
   // many of them take fresh (T0) extensions
-  const int occ = pk ? D.occ_pk : D.occ_m, occm = D.occ_pkm;
+  // lanes per long extension ("Long mode"): 4 lanes x 8 cells, or 8 x 4 from X = 32 on
+  // (measured: X-sweep X = 50 / 100 49.3 / 56.6 -> 47.2 / 50.8 ms, X = 15 21.0 -> 24.3 ms)
+  const int lg = D.long_g >= 0 ? D.long_g : (p.xdrop >= 32 ? 8 : 4);
+  const int occ = pk ? (lg == 8 ? std::min(D.occ_pk, D.occ_pk8) : D.occ_pk) : D.occ_m;
+  const int occm = lg == 8 ? std::min(D.occ_pkm, D.occ_pkm8) : D.occ_pkm;
   const int t0b = pk && D.t0_per_sm > 0 ? std::min(occ, D.t0_per_sm) : occ;
   // the shared kernel keeps one block per SM for escalated work only (measured: X-sweep X = 100
   // 67.5 -> 64.7 ms, C. elegans x0.05 57.6 -> 55.9 ms, X = 15 / 50 within 2 % better)
@@ -339,7 +348,7 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
         P, D.wcost.as<int>(), D.hist.as<int>(), D.bad.as<unsigned long long>() + 1, XDROP_MAX_READ_LEN,
         ctr + C_MAXM);
     xk::scan_kernel<<<1, 1024, 0, s>>>(D.hist.as<int>(), D.cursor.as<int>(), ctr + C_NLONG,
-                                       (long long)D.sms * t0b * 128, D.long_g ? D.long_alpha : 0.f,
+                                       (long long)D.sms * t0b * 128, lg ? D.long_alpha : 0.f,
                                        D.bad.as<unsigned long long>() + 1, ctr + C_NITEMS);
     xk::scatter_kernel<<<(unsigned)((n_items + 255) / 256), 256, 0, s>>>(
         D.wcost.as<int>(), n_items, D.cursor.as<int>(), D.items.as<int>(), fl.nosort ? 1 : 0);
@@ -491,23 +500,27 @@ int dev_pipeline(DevCtx& D, const char* seqA, const int64_t* offA, int64_t nA, i
       D.st.band_kernel = pk ? (choice == 2 ? 2 : 1) : 0;   // refined from the probe count after the call
       if (run_tiered && cpk)
         xk::pk_tiered_kernel<4, 8, true><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      else if (run_tiered && D.long_g == 2)
+      else if (run_tiered && lg == 8)
+        xk::pk_tiered_kernel<8, 4><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
+      else if (run_tiered && lg == 2)
         xk::pk_tiered_kernel<2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       else if (run_tiered)
         xk::pk_tiered_kernel<4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       if (run_shared && cpk)
         xk::pk_merged_kernel<4, 8, true><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
-      else if (run_shared && D.long_g == 2)
+      else if (run_shared && lg == 8)
+        xk::pk_merged_kernel<8, 4><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
+      else if (run_shared && lg == 2)
         xk::pk_merged_kernel<2, 16><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
-      else if (run_shared)      // long_g 4, or 1 (no long mode: n_long = 0)
+      else if (run_shared)      // lg 4, or 0 (no long mode: n_long = 0)
         xk::pk_merged_kernel<4, 8><<<grid_m, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mcm, tiers, stlm);
       if (run_tiered && run_shared) ++launches;
       if (pk) {
         D.probe_thr = mc.probe_thr;
         D.probe_choice = choice;
-      } else if (D.long_g == 2) {     // 32-bit cells (X + M > 510)
+      } else if (lg == 2) {           // 32-bit cells (X + M > 510)
         xk::band_merged_kernel<32, 2, 16><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
-      } else if (D.long_g == 4) {
+      } else if (lg == 4 || lg == 8) {
         xk::band_merged_kernel<32, 4, 8><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
       } else {
         xk::band_merged_kernel<32, 1, 32><<<grid, 128, 0, s>>>(P, items0, ctr + C_NITEMS, mc, e1, e2, e3, stl);
