@@ -46,6 +46,16 @@ def build_checked(force: bool = False, verbose: bool = False) -> str:
     return _build_one(OUT_CHECKED, ["-DXDROP_CHECKED"], force, verbose)
 
 
+def build_all(force: bool = False, verbose: bool = False) -> tuple:
+    """libxdrop.so and libxdrop_checked.so, the two nvcc runs concurrently (each is one big
+    translation unit, so this halves the wall time of a clean build)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        a = ex.submit(build, force, verbose)
+        c = ex.submit(build_checked, force, verbose)
+        return a.result(), c.result()
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
     if "--checked" in sys.argv:
